@@ -1,0 +1,382 @@
+"""Benchmark: transform coefficients/s (forward + inverse each counted) of the
+adjusted-transform hot path on B200, with the roofline and the reference CPU
+path beside it.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl ours|reference]
+
+Default workload (BASELINE.json configs[1], the config the metric is quoted on
+that fits one GPU): 65,536 blocks of 32x32 fp32 integer residuals (AR(1)
+rho=0.85, sigma=24, clipped to [-512, 511]), forward + inverse DCT-8
+approximation = DCT-2 butterfly + designed 8x8 post-adjustment on both axes.
+One step = forward_adjusted_2d then inverse_adjusted_2d over the batch, each one
+fused kernel (rows + columns + adjustment).  Inputs are 268 MB per GPU (> the
+126 MB L2), so no flush is needed between steps.
+
+Multi-GPU (torchrun): every rank runs the same per-GPU workload on its own
+block range (weak scaling, no data-path collective); timing is CUDA events on
+the launching stream, max over ranks (NCCL all_reduce of scalars only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "transform coeffs/sec (fwd+inv) at 1/2/4/8 B200; % of HBM roofline vs CPU ref"
+UNIT = "coef/s"
+
+
+# ------------------------------------------------------------------ configs
+def _c2_transforms():
+    from paper_2505_23618_b200 import matio, pipeline
+    from paper_2505_23618_b200.design import dct8_adjustment_from_dst7
+    t = pipeline.make_adjusted_transform(
+        dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32")))
+    return t, t
+
+
+def _c1_transforms():
+    from paper_2505_23618_b200 import matio, pipeline
+    t = pipeline.make_adjusted_transform(matio.load_designed("band6_pre_dst3_dst7_n32"))
+    return t, t
+
+
+def _c4_transforms(variant):
+    from paper_2505_23618_b200 import matio, pipeline
+    from paper_2505_23618_b200.design import dct8_adjustment_from_dst7, flip_pre_adjustment
+    b6 = matio.load_designed("band6_pre_dst3_dst7_n64")
+    s7 = matio.load_designed("sub8_post_dct2_dst7_n64")
+    adj = {"dst7_pre": b6, "dct8_pre": flip_pre_adjustment(b6), "dst7_post": s7,
+           "dct8_post": dct8_adjustment_from_dst7(s7)}[variant]
+    t = pipeline.make_adjusted_transform(adj)
+    return t, t
+
+
+CONFIGS = {
+    "c2": dict(workload="c2_dct8_post_sub8_n32_fwd+inv_65536x32x32", blocks=65536, h=32, w=32,
+               dtype="f32", transforms=_c2_transforms, inputs="c2_inputs", inverse=True),
+    "c1": dict(workload="c1_dst7_pre_band6_n32_fwd_4096x32x32", blocks=4096, h=32, w=32,
+               dtype="f64", transforms=_c1_transforms, inputs="c1_inputs", inverse=False),
+}
+for _v in ("dst7_pre", "dct8_pre", "dst7_post", "dct8_post"):
+    CONFIGS[f"c4_{_v}"] = dict(workload=f"c4_{_v}_n64_fwd+inv_262144x64x64", blocks=262144, h=64,
+                               w=64, dtype="f32", transforms=(lambda v=_v: _c4_transforms(v)),
+                               inputs="c4_inputs", inverse=True)
+
+
+def _oaxis(t):
+    from oracle import oracle as O
+    adj = t.adjustment
+    base = {"dct2": O.BASE_DCT2, "dst3": O.BASE_DST3, "dct3": O.BASE_DCT3}[adj.base.value]
+    kind = {"band": O.ADJ_BAND, "subblock": O.ADJ_SUBBLOCK, "dense": O.ADJ_DENSE}[adj.pattern.kind.value]
+    return O.OAxis(adj.pattern.size, base, kind, O.SIDE_PRE if adj.side.value == "pre" else O.SIDE_POST,
+                   adj.pattern.taps or 0, adj.pattern.order or 0, np.array(adj.realized))
+
+
+# ------------------------------------------------------------------ helpers
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _traffic(workload: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(workload)
+    return None
+
+
+# ------------------------------------------------------------------ CPU legs
+def _cpu_worker(args):
+    kind, cfg_name, nblk, seed, reps = args
+    import numpy as np  # noqa: F811
+    from oracle import oracle as O
+    cfg = CONFIGS[cfg_name]
+    th, tv = cfg["transforms"]()
+    ah, av = _oaxis(th), _oaxis(tv)
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((nblk, cfg["h"], cfg["w"])) * 24.0
+    if kind == "reference":
+        ref = O.RefPipeline()
+        fwd = lambda a: ref.forward_2d(ah, av, a)  # noqa: E731
+        inv = lambda a: ref.inverse_2d(ah, av, a)  # noqa: E731
+    else:
+        fwd = lambda a: O.adjusted_2d(ah, av, a)  # noqa: E731
+        inv = lambda a: O.adjusted_2d(ah, av, a, inverse=True)  # noqa: E731
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        y = fwd(x)
+        if cfg["inverse"]:
+            inv(y)
+    return time.perf_counter() - t0
+
+
+def cpu_throughput(cfg_name: str, seconds: float = 10.0):
+    """Reference CPU path on this host's cores: the reference's compiled core
+    (oracle/_ref, kind "reference") when built, else the C port (kind "port");
+    one process per core, each on its own contiguous block sample."""
+    from multiprocessing import get_context
+    from oracle import oracle as O
+    cfg = CONFIGS[cfg_name]
+    kind = "reference" if O.ref_fastcore() is not None else "port"
+    cores = O.threads_available()
+    nblk = 256 if cfg["h"] == 32 else 64
+    per_pass = nblk * cfg["h"] * cfg["w"] * (2 if cfg["inverse"] else 1)
+    # calibrate one worker
+    t1 = _cpu_worker((kind, cfg_name, nblk, 0, 1))
+    reps = max(1, int(seconds / max(t1, 1e-6)))
+    with get_context("fork").Pool(cores) as pool:
+        times = pool.map(_cpu_worker, [(kind, cfg_name, nblk, s, reps) for s in range(cores)])
+    value = cores * reps * per_pass / max(times)
+    sample = (f"{cores} processes x {reps} passes x {nblk} blocks ({cfg['h']}x{cfg['w']}, "
+              f"{'fwd+inv' if cfg['inverse'] else 'fwd'}) of the {cfg_name} workload")
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    per = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_throughput(args.config, seconds=4.0)
+        if i >= args.warmup:
+            per.append(r["value"])
+            res = r
+    value = float(np.median(per))
+    res["value"] = value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": cfg["workload"], "sample_per_step": res["sample"]},
+            "cpu_baseline": res,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_23618_b200 import pipeline, workloads
+    from paper_2505_23618_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = CONFIGS[args.config]
+    th, tv = cfg["transforms"]()
+    nblk = cfg["blocks"]
+    x = getattr(workloads, cfg["inputs"])("cuda", nblk, offset=rank * nblk)
+    y = torch.empty_like(x)
+    xr = torch.empty_like(x)
+    es = x.element_size()
+    coef = nblk * cfg["h"] * cfg["w"]
+
+    # oracle gate before timing (reference benchmark.py:181-190)
+    from oracle import oracle as O
+    y0 = pipeline.forward_adjusted_2d(th, tv, x)
+    idx = torch.arange(0, nblk, max(1, nblk // 256), device="cuda")
+    xs = x[idx].cpu().numpy().astype(np.float64)
+    ys = O.adjusted_2d(_oaxis(th), _oaxis(tv), xs)
+    err = float((np.abs(y0[idx].cpu().numpy() - ys).reshape(len(idx), -1).max(1)
+                 / np.maximum(np.abs(ys).reshape(len(idx), -1).max(1), 1e-300)).max())
+    tol = 1e-5 if cfg["dtype"] == "f32" else 1e-9
+    if err > tol:
+        raise SystemExit(f"oracle gate failed: rel err {err:.3e} > {tol}")
+    del y0
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        _fwd(x, y)
+        if cfg["inverse"]:
+            _inv(y, xr)
+
+    import ctypes
+    (axh, keep_h), (axv, keep_v) = th.axis(), tv.axis()
+    dt = _lib.F32 if x.dtype == torch.float32 else _lib.F64
+    lib = _lib.load()
+
+    def _fwd(a, b):
+        _lib.check(lib.dctadj_forward_2d(ctypes.byref(axh), ctypes.byref(axv), a.data_ptr(),
+                                         b.data_ptr(), nblk, dt, stream.cuda_stream))
+
+    def _inv(a, b):
+        _lib.check(lib.dctadj_inverse_2d(ctypes.byref(axh), ctypes.byref(axv), a.data_ptr(),
+                                         b.data_ptr(), nblk, dt, stream.cuda_stream))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    n_ev = 3 if cfg["inverse"] else 2
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            evs[k][0].record(stream)
+            _fwd(x, y)
+            evs[k][1].record(stream)
+            if cfg["inverse"]:
+                _inv(y, xr)
+                evs[k][2].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    inv_ms = [e[1].elapsed_time(e[2]) for e in evs] if cfg["inverse"] else []
+    total_ms = evs[0][0].elapsed_time(evs[-1][-1])
+
+    # e2e through the host-buffer C-ABI entries (pinned host memory, copies inside)
+    xh = x.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    xrh = torch.empty_like(xh).pin_memory()
+    xh_np, yh_np, xrh_np = xh.numpy(), yh.numpy(), xrh.numpy()
+    e2e_steps = max(2, min(args.steps, 5))
+    for _ in range(1):
+        pipeline.forward_adjusted_2d_host(th, tv, xh_np, out=yh_np)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        pipeline.forward_adjusted_2d_host(th, tv, xh_np, out=yh_np)
+        if cfg["inverse"]:
+            pipeline.inverse_adjusted_2d_host(th, tv, yh_np, out=xrh_np)
+    e2e_s = time.perf_counter() - t0
+    if cfg["inverse"] and not np.array_equal(np.rint(xrh_np), xh_np) and cfg["inputs"] == "c2_inputs":
+        raise SystemExit("e2e round trip lost integer exactness")
+
+    if world > 1:
+        t = torch.tensor([total_ms, e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_s = float(t[0]), float(t[1])
+
+    per_step_coef = coef * (2 if cfg["inverse"] else 1)
+    ms_per_step = total_ms / args.steps
+    value = world * per_step_coef / (ms_per_step / 1e3)
+    e2e_value = world * per_step_coef * e2e_steps / e2e_s
+    bytes_per_launch = 2 * coef * es  # read x once, write y once
+    fwd_avg = float(np.mean(fwd_ms))
+    peak, peak_src = _peaks()
+    achieved = bytes_per_launch / (fwd_avg / 1e3) / 1e9
+    traffic = _traffic(cfg["workload"])
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (seeded AR(1) residual blocks, SURVEY.md App. A D12)",
+        "config": {"workload": cfg["workload"], "blocks_per_gpu": nblk,
+                   "block": f"{cfg['h']}x{cfg['w']}",
+                   "l2": f"inputs {coef * es / 1e6:.0f} MB per GPU > 126 MB L2; no flush",
+                   "parallelism": f"block-range shards x{world}",
+                   "oracle_gate_rel_err": err},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "tile_kernel forward (fused rows+cols+adjustment)",
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "avg_launch_ms": fwd_avg,
+                     "inverse_avg_launch_ms": float(np.mean(inv_ms)) if inv_ms else None},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step":
+                coef * es * (2 if cfg["inverse"] else 1),
+                "d2h_bytes_per_step": coef * es * (2 if cfg["inverse"] else 1),
+                "api": "forward_adjusted_2d_host / inverse_adjusted_2d_host (C-ABI *_2d_host)"},
+        "gpu_launches": args.steps * (2 if cfg["inverse"] else 1),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_throughput(args.config, seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

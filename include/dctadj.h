@@ -1,0 +1,133 @@
+/*
+ * dctadj.h -- C-ABI of the B200 adjusted-transform engine (libdctadj.so).
+ *
+ * Drop-in boundary for the reference's kernel plugin API
+ * (reference pkg/src/dctadjust/kernels/__init__.py:33-41, a backend module
+ * exporting dct2/idct2/dst3/idst3/band/subblock/dense over (nvec, N) batches)
+ * and for its pipeline entry points forward_adjusted / inverse_adjusted
+ * (reference pkg/src/dctadjust/pipeline.py:176-191).  The 2-D, frame and mixed
+ * entries have no reference counterpart: they fuse the reference's 2-D
+ * composition (rows then columns, pipeline.py:236-239) into one kernel.
+ *
+ * Conventions
+ *  - Plain C types only.  `x`/`y` are DEVICE pointers (row-major, contiguous)
+ *    unless the name ends in _host; `stream` is a cudaStream_t (NULL = legacy
+ *    default stream).  Calls are stream-ordered, reentrant and never block the
+ *    host, except the *_host entries, which return when the host output is
+ *    written.
+ *  - Adjustment matrices (`a`, `blk`, `m`, dctadj_axis.mat) are HOST float64
+ *    arrays, read during the call (packed into the launch), never retained.
+ *  - dtype: DCTADJ_F32 or DCTADJ_F64; inputs and outputs share it.
+ *  - Outputs are caller-allocated and must not alias inputs.
+ *  - Return value: DCTADJ_OK or an error code; no exception crosses the ABI.
+ *    Codes map 1:1 onto the reference's error classes (errors.py:4-37):
+ *    DIMENSION->InvalidDimensionError, SHAPE->ShapeError,
+ *    PATTERN->PatternError, CONFIG->ConfigurationError,
+ *    KIND->KindMismatchError, VALUE->ValueError.  dctadj_last_error() returns
+ *    the calling thread's last message.
+ */
+#ifndef DCTADJ_H_
+#define DCTADJ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum dctadj_status {
+  DCTADJ_OK = 0,
+  DCTADJ_ERR_DIMENSION = 1,   /* InvalidDimensionError (pipeline.py:40-44) */
+  DCTADJ_ERR_SHAPE = 2,       /* ShapeError (pipeline.py:47-57) */
+  DCTADJ_ERR_PATTERN = 3,     /* PatternError (pipeline.py:92-104) */
+  DCTADJ_ERR_CONFIG = 4,      /* ConfigurationError (pipeline.py:141-148) */
+  DCTADJ_ERR_KIND = 5,        /* KindMismatchError (errors.py:16-17) */
+  DCTADJ_ERR_CUDA = 6,        /* CUDA runtime / driver failure */
+  DCTADJ_ERR_UNSUPPORTED = 7, /* no kernel for this configuration */
+  DCTADJ_ERR_VALUE = 8        /* ValueError (e.g. N > 64, _fastcore.pyx:194-195) */
+};
+
+enum dctadj_dtype { DCTADJ_F32 = 0, DCTADJ_F64 = 1 };
+
+/* base transform of one axis (reference transforms.py TransformKind) */
+enum dctadj_base {
+  DCTADJ_BASE_DCT2 = 0, /* FAST_DCT2 (pipeline.py:35-37) */
+  DCTADJ_BASE_DST3 = 1, /* FAST_DST3_VIA_DCT2 */
+  DCTADJ_BASE_DCT3 = 2  /* DCT-3 = DCT-2^T: the DCT-8 pre flip */
+};
+/* adjustment pattern kind (reference design.py:43-46) and side (design.py:49-51) */
+enum dctadj_adj { DCTADJ_ADJ_NONE = 0, DCTADJ_ADJ_BAND = 1, DCTADJ_ADJ_SUBBLOCK = 2,
+                  DCTADJ_ADJ_DENSE = 3 };
+enum dctadj_side { DCTADJ_SIDE_PRE = 0, DCTADJ_SIDE_POST = 1 };
+
+/* One axis of an adjusted transform: the reference AdjustedTransform
+ * (pipeline.py:127-135) flattened to plain data. */
+typedef struct dctadj_axis {
+  int32_t n;          /* transform length: 4, 8, 16, 32 or 64 (FAST_SIZES) */
+  int32_t base;       /* dctadj_base */
+  int32_t adj;        /* dctadj_adj */
+  int32_t side;       /* dctadj_side */
+  int32_t taps;       /* band taps (adj == BAND) */
+  int32_t order;      /* sub-block order (adj == SUBBLOCK) */
+  const double* mat;  /* host n x n realized adjustment (row-major); NULL if NONE */
+} dctadj_axis;
+
+/* ---- the seven batch primitives (reference kernels/__init__.py:33-41) ----
+ * x, y: (nvec, n) row-major device arrays. */
+int dctadj_dct2(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype, void* stream);
+int dctadj_idct2(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype, void* stream);
+int dctadj_dst3(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype, void* stream);
+int dctadj_idst3(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype, void* stream);
+/* y[i,r] = sum_{|r-j|<taps} a[r,j] x[i,j]; a: host n x n  (_fastcore.pyx:253-273) */
+int dctadj_band(const double* a, int32_t taps, const void* x, void* y, int64_t nvec, int32_t n,
+                int32_t dtype, void* stream);
+/* y = x with y[i,0:b] = blk x[i,0:b]; blk: host b x b; tail copied (_fastcore.pyx:276-290) */
+int dctadj_subblock(const double* blk, int32_t b, const void* x, void* y, int64_t nvec,
+                    int32_t n, int32_t dtype, void* stream);
+/* y (nvec, rows) = x m^T; m: host rows x n  (_fastcore.pyx:293-307) */
+int dctadj_dense(const double* m, int32_t rows, const void* x, void* y, int64_t nvec, int32_t n,
+                 int32_t dtype, void* stream);
+
+/* ---- fused 1-D adjusted transforms (pipeline.py:176-191) ---- */
+int dctadj_forward_1d(const dctadj_axis* ax, const void* x, void* y, int64_t nvec, int32_t dtype,
+                      void* stream);
+int dctadj_inverse_1d(const dctadj_axis* ax, const void* y, void* x, int64_t nvec, int32_t dtype,
+                      void* stream);
+
+/* ---- fused 2-D separable transforms over (nblk, H, W) blocks ----
+ * h: row axis (length W), v: column axis (length H).
+ * forward: Y = T_v X T_h^T (rows, then columns); inverse: X = T_v^T Y T_h. */
+int dctadj_forward_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
+                      int64_t nblk, int32_t dtype, void* stream);
+int dctadj_inverse_2d(const dctadj_axis* h, const dctadj_axis* v, const void* y, void* x,
+                      int64_t nblk, int32_t dtype, void* stream);
+
+/* Host-buffer variants: x_host/y_host are host arrays (pinned for full speed);
+ * copies, kernels and read-back are pipelined over chunks on internal streams.
+ * Blocks until y_host is written.  device: CUDA ordinal to run on. */
+int dctadj_forward_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x_host,
+                           void* y_host, int64_t nblk, int32_t dtype, int32_t device);
+int dctadj_inverse_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* y_host,
+                           void* x_host, int64_t nblk, int32_t dtype, int32_t device);
+
+/* ---- frame tiling: frames (nframes, height, width) <-> block-major
+ * coefficients (nframes * ceil(height/H) * (width/W), H, W).  Rows past
+ * `height` are zero padding on the way in and clipped on the way out. */
+int dctadj_forward_frames(const dctadj_axis* h, const dctadj_axis* v, const void* frames,
+                          void* coefs, int32_t nframes, int32_t height, int32_t width,
+                          int32_t dtype, void* stream);
+int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void* coefs,
+                          void* frames, int32_t nframes, int32_t height, int32_t width,
+                          int32_t dtype, void* stream);
+
+/* ---- diagnostics ---- */
+const char* dctadj_status_string(int32_t status);
+const char* dctadj_last_error(void);
+int32_t dctadj_version(void);
+/* number of tile_kernel instantiations compiled into this library */
+int32_t dctadj_kernel_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCTADJ_H_ */

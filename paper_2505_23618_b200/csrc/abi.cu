@@ -1,0 +1,669 @@
+// abi.cu -- the C-ABI (include/dctadj.h): validation with the reference's error
+// semantics, per-axis planning (stage codes + packed coefficients), kernel
+// dispatch over the generated instantiation table, TMA tensor-map encoding, and
+// the pipelined host-buffer entry points.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "../../include/dctadj.h"
+#include "launch.cuh"
+
+namespace dctadj {
+
+struct KernelEntry {
+  int dtype, h, w, rc, cc, col_first, in_mode, out_mode;
+  int (*fn)(const LaunchArgs&);
+};
+
+#include "gen/registry.inc"
+
+static_assert(ST_ERR_DIMENSION == DCTADJ_ERR_DIMENSION && ST_ERR_VALUE == DCTADJ_ERR_VALUE,
+              "status codes drifted from include/dctadj.h");
+
+static thread_local char g_err[512] = "";
+
+void set_last_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define DA_CUDA(call)                                                           \
+  do {                                                                          \
+    cudaError_t e_ = (call);                                                    \
+    if (e_ != cudaSuccess)                                                      \
+      return fail(ST_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_));        \
+  } while (0)
+
+// ------------------------------------------------------------- tensor maps
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+int encode_tensor_map(CUtensorMap* map, int dtype, int rank, const uint64_t* dims,
+                      const uint64_t* strides_bytes, const uint32_t* box, int box_row_bytes,
+                      void* base) {
+  EncodeFn fn = get_encode();
+  if (!fn) return fail(ST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i + 1 < rank) s[i] = strides_bytes[i];
+  }
+  CUtensorMapSwizzle swz = box_row_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : box_row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                           : box_row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                 : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = fn(map, dtype == DT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                  rank, base, d, s, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): rank %d dims %llu x %llu",
+                (int)r, rank, (unsigned long long)d[0], (unsigned long long)d[1]);
+  return ST_OK;
+}
+
+int num_sms_cached() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 1;
+  }
+  return cache[dev];
+}
+
+static const KernelEntry* find_kernel(int dtype, int h, int w, int rc, int cc, int col_first,
+                                      int in_mode, int out_mode) {
+  for (const KernelEntry& e : kRegistry)
+    if (e.dtype == dtype && e.h == h && e.w == w && e.rc == rc && e.cc == cc &&
+        e.col_first == col_first && e.in_mode == in_mode && e.out_mode == out_mode)
+      return &e;
+  return nullptr;
+}
+
+// ------------------------------------------------------------- axis planning
+static bool fast_size(int n) { return n == 4 || n == 8 || n == 16 || n == 32 || n == 64; }
+
+// exact base matrices from the closed forms (reference transforms.py:78-120)
+static void base_matrix(int base, int n, std::vector<double>& m) {
+  m.assign(static_cast<size_t>(n) * n, 0.0);
+  std::vector<double> c2(static_cast<size_t>(n) * n);
+  const double pi = 3.141592653589793238462643383279502884;
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j) {
+      double v = std::cos(pi * k * (2 * j + 1) / (2.0 * n)) * std::sqrt(2.0 / n);
+      if (k == 0) v *= 0.7071067811865476;
+      c2[k * n + j] = v;
+    }
+  for (int r = 0; r < n; ++r)
+    for (int j = 0; j < n; ++j) {
+      if (base == DCTADJ_BASE_DCT2)
+        m[r * n + j] = c2[r * n + j];
+      else if (base == DCTADJ_BASE_DCT3)
+        m[r * n + j] = c2[j * n + r];
+      else  // DST3 = S * DCT2^T * R: (r, j) -> (-1)^r DCT2[n-1-j][r]
+        m[r * n + j] = ((r & 1) ? -1.0 : 1.0) * c2[(n - 1 - j) * n + r];
+    }
+}
+
+struct AxisPlan {
+  int n = 0;
+  int code = 0;
+  int gain_sq = 1;
+  std::vector<double> coef;   // packed band / sub-block coefficients (fp64)
+  std::vector<double> dense;  // n x n for ST_DENSE
+};
+
+static int validate_axis(const dctadj_axis* ax) {
+  if (!ax) return fail(ST_ERR_VALUE, "axis descriptor is NULL");
+  if (!fast_size(ax->n))
+    return fail(ST_ERR_DIMENSION, "fast transforms support sizes (4, 8, 16, 32, 64), got %d",
+                ax->n);
+  if (ax->base < DCTADJ_BASE_DCT2 || ax->base > DCTADJ_BASE_DCT3)
+    return fail(ST_ERR_CONFIG, "no fast path for base transform %d; use dct2, dst3 or dct3",
+                ax->base);
+  if (ax->adj < DCTADJ_ADJ_NONE || ax->adj > DCTADJ_ADJ_DENSE)
+    return fail(ST_ERR_PATTERN, "unknown adjustment kind %d", ax->adj);
+  if (ax->side != DCTADJ_SIDE_PRE && ax->side != DCTADJ_SIDE_POST)
+    return fail(ST_ERR_CONFIG, "unknown adjustment side %d", ax->side);
+  if (ax->adj != DCTADJ_ADJ_NONE && !ax->mat)
+    return fail(ST_ERR_VALUE, "adjustment matrix pointer is NULL");
+  if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps < 1 || ax->taps > ax->n))
+    return fail(ST_ERR_PATTERN, "band taps must be in 1..%d, got %d", ax->n, ax->taps);
+  if (ax->adj == DCTADJ_ADJ_SUBBLOCK && (ax->order < 1 || ax->order > ax->n))
+    return fail(ST_ERR_PATTERN, "sub-block order must be in 1..%d, got %d", ax->n, ax->order);
+  return ST_OK;
+}
+
+static double mat_at(const dctadj_axis* ax, bool transpose, int r, int j) {
+  const int n = ax->n;
+  return transpose ? ax->mat[j * n + r] : ax->mat[r * n + j];
+}
+
+// The whole axis as one dense matrix (forward H = B*A or C*B; inverse H^T).
+static void composite_dense(const dctadj_axis* ax, bool inverse, std::vector<double>& out) {
+  const int n = ax->n;
+  std::vector<double> b, a(static_cast<size_t>(n) * n, 0.0), h(static_cast<size_t>(n) * n, 0.0);
+  base_matrix(ax->base, n, b);
+  for (int r = 0; r < n; ++r)
+    for (int j = 0; j < n; ++j) {
+      double v;
+      if (ax->adj == DCTADJ_ADJ_NONE) {
+        v = (r == j) ? 1.0 : 0.0;
+      } else if (ax->adj == DCTADJ_ADJ_BAND) {  // only in-band entries are read (_fastcore.pyx:261-272)
+        v = (std::abs(r - j) < ax->taps) ? ax->mat[r * n + j] : 0.0;
+      } else if (ax->adj == DCTADJ_ADJ_SUBBLOCK) {  // identity outside the leading block
+        v = (r < ax->order && j < ax->order) ? ax->mat[r * n + j] : (r == j ? 1.0 : 0.0);
+      } else {
+        v = ax->mat[r * n + j];
+      }
+      a[r * n + j] = v;
+    }
+  const bool pre = ax->side == DCTADJ_SIDE_PRE;
+  for (int r = 0; r < n; ++r)
+    for (int j = 0; j < n; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < n; ++k) acc += pre ? b[r * n + k] * a[k * n + j] : a[r * n + k] * b[k * n + j];
+      h[r * n + j] = acc;
+    }
+  out.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int r = 0; r < n; ++r)
+    for (int j = 0; j < n; ++j) out[r * n + j] = inverse ? h[j * n + r] : h[r * n + j];
+}
+
+static void pack_band(const dctadj_axis* ax, bool transpose, int k, std::vector<double>& c) {
+  const int n = ax->n, d = 2 * k - 1;
+  c.assign(static_cast<size_t>(n) * d, 0.0);
+  for (int r = 0; r < n; ++r)
+    for (int t = 0; t < d; ++t) {
+      const int j = r - (k - 1) + t;
+      if (j >= 0 && j < n && std::abs(r - j) < ax->taps) c[r * d + t] = mat_at(ax, transpose, r, j);
+    }
+}
+
+static void pack_sub(const dctadj_axis* ax, bool transpose, int k, std::vector<double>& c) {
+  c.assign(static_cast<size_t>(k) * k, 0.0);
+  for (int r = 0; r < k; ++r)
+    for (int j = 0; j < k; ++j) c[r * k + j] = mat_at(ax, transpose, r, j);
+}
+
+// Stage codes for one axis.  force_dense: plan the dense composite instead.
+static int plan_axis(const dctadj_axis* ax, bool inverse, bool force_dense, AxisPlan* p) {
+  int rc = validate_axis(ax);
+  if (rc) return rc;
+  p->n = ax->n;
+  p->coef.clear();
+  p->dense.clear();
+  const int bf = ax->base == DCTADJ_BASE_DCT2 ? ST_DCT2 : ax->base == DCTADJ_BASE_DST3 ? ST_DST3 : ST_IDCT2;
+  const int bi = ax->base == DCTADJ_BASE_DCT2 ? ST_IDCT2 : ax->base == DCTADJ_BASE_DST3 ? ST_IDST3 : ST_DCT2;
+  const int base = inverse ? bi : bf;
+  int adj_stage = ST_NONE, k = 0;
+  if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps == 4 || ax->taps == 6)) {
+    adj_stage = ST_BAND;
+    k = ax->taps;
+    pack_band(ax, inverse, k, p->coef);
+  } else if (ax->adj == DCTADJ_ADJ_SUBBLOCK && ax->order == 8) {
+    adj_stage = ST_SUB;
+    k = 8;
+    pack_sub(ax, inverse, k, p->coef);
+  } else if (ax->adj != DCTADJ_ADJ_NONE) {
+    force_dense = true;
+  }
+  if (force_dense) {
+    composite_dense(ax, inverse, p->dense);
+    p->code = op_code(ST_DENSE);
+    p->gain_sq = 1;
+    p->coef.clear();
+    return ST_OK;
+  }
+  p->gain_sq = ax->n;
+  if (adj_stage == ST_NONE)
+    p->code = op_code(base);
+  else if ((ax->side == DCTADJ_SIDE_PRE) != inverse)  // fwd PRE or inv POST: adjustment first
+    p->code = op_code(adj_stage, base, k);
+  else
+    p->code = op_code(base, adj_stage, k);
+  return ST_OK;
+}
+
+static size_t dt_size(int dtype) { return dtype == DT_F32 ? 4 : 8; }
+
+// fp64 host coefficients -> the kernel's element type
+static std::vector<unsigned char> to_dtype(const std::vector<double>& v, int dtype) {
+  std::vector<unsigned char> out(v.size() * dt_size(dtype) + 8);
+  if (dtype == DT_F32) {
+    float* f = reinterpret_cast<float*>(out.data());
+    for (size_t i = 0; i < v.size(); ++i) f[i] = static_cast<float>(v[i]);
+  } else {
+    std::memcpy(out.data(), v.data(), v.size() * sizeof(double));
+  }
+  return out;
+}
+
+// stream-ordered device copy of a dense matrix; freed with free_dense after use
+static int upload_dense(const AxisPlan& p, int dtype, cudaStream_t st, void** dev) {
+  *dev = nullptr;
+  if (p.dense.empty()) return ST_OK;
+  std::vector<unsigned char> host = to_dtype(p.dense, dtype);
+  const size_t bytes = p.dense.size() * dt_size(dtype);
+  DA_CUDA(cudaMallocAsync(dev, bytes, st));
+  DA_CUDA(cudaMemcpyAsync(*dev, host.data(), bytes, cudaMemcpyHostToDevice, st));
+  // pageable source: the runtime has staged it before returning, so `host` may die
+  return ST_OK;
+}
+
+struct Launch {
+  const KernelEntry* k = nullptr;
+  LaunchArgs a;
+  std::vector<unsigned char> row_coef, col_coef;
+  void* dense_row = nullptr;
+  void* dense_col = nullptr;
+};
+
+static int prepare(Launch& L, const AxisPlan& row, const AxisPlan* col, int dtype, int h, int w,
+                   bool col_first, int in_mode, int out_mode, cudaStream_t st) {
+  const int cc = col ? col->code : op_code(ST_NONE);
+  L.k = find_kernel(dtype, h, w, row.code, cc, col_first ? 1 : 0, in_mode, out_mode);
+  if (!L.k) return ST_ERR_UNSUPPORTED;
+  L.row_coef = to_dtype(row.coef, dtype);
+  if (col) L.col_coef = to_dtype(col->coef, dtype);
+  int rc = upload_dense(row, dtype, st, &L.dense_row);
+  if (rc) return rc;
+  if (col) {
+    rc = upload_dense(*col, dtype, st, &L.dense_col);
+    if (rc) return rc;
+  }
+  L.a.row_coef = L.row_coef.data();
+  L.a.col_coef = col ? L.col_coef.data() : nullptr;
+  L.a.dense_row = L.dense_row;
+  L.a.dense_col = L.dense_col;
+  L.a.stream = st;
+  return ST_OK;
+}
+
+static int finish(Launch& L, cudaStream_t st) {
+  if (L.dense_row) DA_CUDA(cudaFreeAsync(L.dense_row, st));
+  if (L.dense_col) DA_CUDA(cudaFreeAsync(L.dense_col, st));
+  L.dense_row = L.dense_col = nullptr;
+  return ST_OK;
+}
+
+static int check_dtype(int dtype) {
+  if (dtype != DT_F32 && dtype != DT_F64)
+    return fail(ST_ERR_VALUE, "dtype must be DCTADJ_F32 or DCTADJ_F64, got %d", dtype);
+  return ST_OK;
+}
+
+// ------------------------------------------------------------- 1-D batches
+static int run_1d(const AxisPlan& plan, const void* x, void* y, int64_t nvec, int dtype,
+                  cudaStream_t st) {
+  if (nvec < 0) return fail(ST_ERR_SHAPE, "negative batch size %lld", (long long)nvec);
+  if (nvec == 0) return ST_OK;
+  if (!x || !y) return fail(ST_ERR_VALUE, "NULL data pointer");
+  Launch L;
+  int rc = prepare(L, plan, nullptr, dtype, 32, plan.n, false, MODE_LINEAR, MODE_LINEAR, st);
+  if (rc == ST_ERR_UNSUPPORTED)
+    return fail(rc, "no 1-D kernel for op 0x%x at n=%d dtype=%d", plan.code, plan.n, dtype);
+  if (rc) return rc;
+  L.a.in = x;
+  L.a.out = y;
+  L.a.rows = nvec;
+  rc = L.k->fn(L.a);
+  int rc2 = finish(L, st);
+  return rc ? rc : rc2;
+}
+
+static int run_axis_1d(const dctadj_axis* ax, bool inverse, const void* x, void* y, int64_t nvec,
+                       int dtype, cudaStream_t st) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  AxisPlan p;
+  rc = plan_axis(ax, inverse, false, &p);
+  if (rc) return rc;
+  if (!find_kernel(dtype, 32, p.n, p.code, op_code(ST_NONE), 0, 0, 0)) {
+    rc = plan_axis(ax, inverse, true, &p);
+    if (rc) return rc;
+  }
+  return run_1d(p, x, y, nvec, dtype, st);
+}
+
+static int primitive(int stage, const void* x, void* y, int64_t nvec, int n, int dtype,
+                     cudaStream_t st) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if (n > 64) return fail(ST_ERR_VALUE, "size %d exceeds compiled kernel limit 64", n);
+  if (!fast_size(n))
+    return fail(ST_ERR_DIMENSION, "fast transforms support sizes (4, 8, 16, 32, 64), got %d", n);
+  AxisPlan p;
+  p.n = n;
+  p.code = op_code(stage);
+  p.gain_sq = n;
+  return run_1d(p, x, y, nvec, dtype, st);
+}
+
+// ------------------------------------------------------------- 2-D / frames
+static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
+                  int64_t nblk, int dtype, bool inverse, int in_mode, int out_mode,
+                  int32_t frames, int32_t fh, int32_t fw, cudaStream_t st) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  AxisPlan ph, pv;
+  rc = plan_axis(h, inverse, false, &ph);
+  if (rc) return rc;
+  rc = plan_axis(v, inverse, false, &pv);
+  if (rc) return rc;
+  if (nblk < 0) return fail(ST_ERR_SHAPE, "negative block count %lld", (long long)nblk);
+  if (nblk == 0) return ST_OK;
+  if (!x || !y) return fail(ST_ERR_VALUE, "NULL data pointer");
+  const int H = pv.n, W = ph.n;
+  Launch L;
+  rc = prepare(L, ph, &pv, dtype, H, W, inverse, in_mode, out_mode, st);
+  if (rc == ST_ERR_UNSUPPORTED) {
+    // dense composite of both axes: one fused kernel per shape is always built
+    rc = plan_axis(h, inverse, true, &ph);
+    if (!rc) rc = plan_axis(v, inverse, true, &pv);
+    if (rc) return rc;
+    L = Launch();
+    rc = prepare(L, ph, &pv, dtype, H, W, inverse, in_mode, out_mode, st);
+    if (rc == ST_ERR_UNSUPPORTED)
+      return fail(rc, "no 2-D kernel for %dx%d blocks, dtype %d (mode %d->%d)", H, W, dtype,
+                  in_mode, out_mode);
+  }
+  if (rc) return rc;
+  L.a.in = x;
+  L.a.out = y;
+  L.a.rows = nblk * H;
+  L.a.frames = frames;
+  L.a.frame_h = fh;
+  L.a.frame_w = fw;
+  rc = L.k->fn(L.a);
+  int rc2 = finish(L, st);
+  return rc ? rc : rc2;
+}
+
+// Host-buffer pipeline: chunks of blocks cycle through NSTREAM streams, each
+// with its own device in/out buffers: H2D(c) overlaps kernel(c-1) and D2H(c-2).
+static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* xh, void* yh,
+                       int64_t nblk, int dtype, bool inverse, int device) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if ((rc = validate_axis(h)) != ST_OK || (rc = validate_axis(v)) != ST_OK) return rc;
+  if (nblk < 0) return fail(ST_ERR_SHAPE, "negative block count %lld", (long long)nblk);
+  if (nblk == 0) return ST_OK;
+  if (!xh || !yh) return fail(ST_ERR_VALUE, "NULL data pointer");
+  DA_CUDA(cudaSetDevice(device));
+  constexpr int NSTREAM = 3;
+  const size_t blk_bytes = static_cast<size_t>(h->n) * v->n * dt_size(dtype);
+  const int64_t chunk = std::max<int64_t>(1, static_cast<int64_t>((32u << 20) / blk_bytes));
+  const int64_t nchunks = (nblk + chunk - 1) / chunk;
+  const int nbuf = static_cast<int>(std::min<int64_t>(NSTREAM, nchunks));
+  cudaStream_t st[NSTREAM] = {};
+  void* din[NSTREAM] = {};
+  void* dout[NSTREAM] = {};
+  int status = ST_OK;
+  for (int i = 0; i < nbuf && !status; ++i) {
+    if (cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMallocAsync(&din[i], chunk * blk_bytes, st[i]) != cudaSuccess ||
+        cudaMallocAsync(&dout[i], chunk * blk_bytes, st[i]) != cudaSuccess)
+      status = fail(ST_ERR_CUDA, "host pipeline setup: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  for (int64_t c = 0; c < nchunks && !status; ++c) {
+    const int k = static_cast<int>(c % nbuf);
+    const int64_t b0 = c * chunk, nb = std::min(chunk, nblk - b0);
+    const size_t off = static_cast<size_t>(b0) * blk_bytes, bytes = static_cast<size_t>(nb) * blk_bytes;
+    if (cudaMemcpyAsync(din[k], static_cast<const char*>(xh) + off, bytes, cudaMemcpyHostToDevice,
+                        st[k]) != cudaSuccess) {
+      status = fail(ST_ERR_CUDA, "H2D copy: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    status = run_2d(h, v, din[k], dout[k], nb, dtype, inverse, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, st[k]);
+    if (status) break;
+    if (cudaMemcpyAsync(static_cast<char*>(yh) + off, dout[k], bytes, cudaMemcpyDeviceToHost,
+                        st[k]) != cudaSuccess)
+      status = fail(ST_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  for (int i = 0; i < nbuf; ++i) {
+    if (!st[i]) continue;
+    if (din[i]) cudaFreeAsync(din[i], st[i]);
+    if (dout[i]) cudaFreeAsync(dout[i], st[i]);
+    cudaError_t e = cudaStreamSynchronize(st[i]);
+    if (e != cudaSuccess && !status) status = fail(ST_ERR_CUDA, "pipeline: %s", cudaGetErrorString(e));
+    cudaStreamDestroy(st[i]);
+  }
+  return status;
+}
+
+static int run_frames(const dctadj_axis* h, const dctadj_axis* v, const void* in, void* out,
+                      int32_t nframes, int32_t height, int32_t width, int dtype, bool inverse,
+                      cudaStream_t st) {
+  if (!h || !v) return fail(ST_ERR_VALUE, "axis descriptor is NULL");
+  if (nframes < 0 || height < 0 || width < 0)
+    return fail(ST_ERR_SHAPE, "negative frame geometry %d x %d x %d", nframes, height, width);
+  if (nframes == 0 || height == 0 || width == 0) return ST_OK;
+  if (width % h->n != 0)
+    return fail(ST_ERR_SHAPE, "frame width %d is not a multiple of the block width %d", width,
+                h->n);
+  const int64_t nblk = static_cast<int64_t>(nframes) * ((height + v->n - 1) / v->n) * (width / h->n);
+  return run_2d(h, v, in, out, nblk, dtype, inverse, inverse ? MODE_LINEAR : MODE_FRAME,
+                inverse ? MODE_FRAME : MODE_LINEAR, nframes, height, width, st);
+}
+
+// generic rectangular dense product (rows != n), the one path off the tile kernel
+template <typename T>
+__global__ void dense_rect_kernel(const T* __restrict__ m, int rows, const T* __restrict__ x,
+                                  T* __restrict__ y, int64_t nvec, int n) {
+  const int64_t total = nvec * rows;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / rows;
+    const int r = static_cast<int>(e - i * rows);
+    T acc = m[r * n] * x[i * n];
+    for (int j = 1; j < n; ++j) acc = fma(m[r * n + j], x[i * n + j], acc);
+    y[e] = acc;
+  }
+}
+
+}  // namespace dctadj
+
+using namespace dctadj;
+
+static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int dctadj_dct2(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype, void* stream) {
+  return primitive(ST_DCT2, x, y, nvec, n, dtype, S(stream));
+}
+int dctadj_idct2(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype, void* stream) {
+  return primitive(ST_IDCT2, x, y, nvec, n, dtype, S(stream));
+}
+int dctadj_dst3(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype, void* stream) {
+  return primitive(ST_DST3, x, y, nvec, n, dtype, S(stream));
+}
+int dctadj_idst3(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype, void* stream) {
+  return primitive(ST_IDST3, x, y, nvec, n, dtype, S(stream));
+}
+
+int dctadj_band(const double* a, int32_t taps, const void* x, void* y, int64_t nvec, int32_t n,
+                int32_t dtype, void* stream) {
+  dctadj_axis ax{n, DCTADJ_BASE_DCT2, DCTADJ_ADJ_BAND, DCTADJ_SIDE_PRE, taps, 0, a};
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  rc = validate_axis(&ax);
+  if (rc) return rc;
+  AxisPlan p;
+  p.n = n;
+  if (taps == 4 || taps == 6) {
+    p.code = op_code(ST_BAND, ST_NONE, taps);
+    pack_band(&ax, false, taps, p.coef);
+    if (find_kernel(dtype, 32, n, p.code, 0, 0, 0, 0)) return run_1d(p, x, y, nvec, dtype, S(stream));
+  }
+  // any other width: the band-masked matrix as a dense product
+  p.code = op_code(ST_DENSE);
+  p.coef.clear();
+  p.dense.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int r = 0; r < n; ++r)
+    for (int j = 0; j < n; ++j)
+      if (std::abs(r - j) < taps) p.dense[r * n + j] = a[r * n + j];
+  return run_1d(p, x, y, nvec, dtype, S(stream));
+}
+
+int dctadj_subblock(const double* blk, int32_t b, const void* x, void* y, int64_t nvec,
+                    int32_t n, int32_t dtype, void* stream) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if (!fast_size(n))
+    return fail(ST_ERR_DIMENSION, "fast transforms support sizes (4, 8, 16, 32, 64), got %d", n);
+  if (b < 1 || b > n) return fail(ST_ERR_PATTERN, "sub-block order must be in 1..%d, got %d", n, b);
+  if (!blk) return fail(ST_ERR_VALUE, "sub-block pointer is NULL");
+  AxisPlan p;
+  p.n = n;
+  if (b == 8) {
+    p.code = op_code(ST_SUB, ST_NONE, 8);
+    p.coef.assign(blk, blk + 64);
+    if (find_kernel(dtype, 32, n, p.code, 0, 0, 0, 0)) return run_1d(p, x, y, nvec, dtype, S(stream));
+  }
+  p.code = op_code(ST_DENSE);
+  p.coef.clear();
+  p.dense.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int r = 0; r < n; ++r) p.dense[r * n + r] = 1.0;
+  for (int r = 0; r < b; ++r)
+    for (int j = 0; j < b; ++j) p.dense[r * n + j] = blk[r * b + j];
+  return run_1d(p, x, y, nvec, dtype, S(stream));
+}
+
+int dctadj_dense(const double* m, int32_t rows, const void* x, void* y, int64_t nvec, int32_t n,
+                 int32_t dtype, void* stream) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if (!m) return fail(ST_ERR_VALUE, "matrix pointer is NULL");
+  if (rows < 1 || n < 1) return fail(ST_ERR_SHAPE, "bad dense shape %d x %d", rows, n);
+  if (nvec < 0) return fail(ST_ERR_SHAPE, "negative batch size");
+  if (nvec == 0) return ST_OK;
+  if (rows == n && fast_size(n)) {
+    AxisPlan p;
+    p.n = n;
+    p.code = op_code(ST_DENSE);
+    p.dense.assign(m, m + static_cast<size_t>(n) * n);
+    return run_1d(p, x, y, nvec, dtype, S(stream));
+  }
+  cudaStream_t st = S(stream);
+  std::vector<double> md(m, m + static_cast<size_t>(rows) * n);
+  AxisPlan p;
+  p.dense = md;
+  void* dm = nullptr;
+  rc = upload_dense(p, dtype, st, &dm);
+  if (rc) return rc;
+  const int64_t total = nvec * rows;
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  if (dtype == DT_F32)
+    dense_rect_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(dm), rows,
+                                                    static_cast<const float*>(x),
+                                                    static_cast<float*>(y), nvec, n);
+  else
+    dense_rect_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(dm), rows,
+                                                     static_cast<const double*>(x),
+                                                     static_cast<double*>(y), nvec, n);
+  DA_CUDA(cudaGetLastError());
+  DA_CUDA(cudaFreeAsync(dm, st));
+  return ST_OK;
+}
+
+int dctadj_forward_1d(const dctadj_axis* ax, const void* x, void* y, int64_t nvec, int32_t dtype,
+                      void* stream) {
+  return run_axis_1d(ax, false, x, y, nvec, dtype, S(stream));
+}
+int dctadj_inverse_1d(const dctadj_axis* ax, const void* y, void* x, int64_t nvec, int32_t dtype,
+                      void* stream) {
+  return run_axis_1d(ax, true, y, x, nvec, dtype, S(stream));
+}
+
+int dctadj_forward_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
+                      int64_t nblk, int32_t dtype, void* stream) {
+  return run_2d(h, v, x, y, nblk, dtype, false, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, S(stream));
+}
+int dctadj_inverse_2d(const dctadj_axis* h, const dctadj_axis* v, const void* y, void* x,
+                      int64_t nblk, int32_t dtype, void* stream) {
+  return run_2d(h, v, y, x, nblk, dtype, true, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, S(stream));
+}
+
+int dctadj_forward_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x_host,
+                           void* y_host, int64_t nblk, int32_t dtype, int32_t device) {
+  return run_2d_host(h, v, x_host, y_host, nblk, dtype, false, device);
+}
+int dctadj_inverse_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* y_host,
+                           void* x_host, int64_t nblk, int32_t dtype, int32_t device) {
+  return run_2d_host(h, v, y_host, x_host, nblk, dtype, true, device);
+}
+
+int dctadj_forward_frames(const dctadj_axis* h, const dctadj_axis* v, const void* frames,
+                          void* coefs, int32_t nframes, int32_t height, int32_t width,
+                          int32_t dtype, void* stream) {
+  return run_frames(h, v, frames, coefs, nframes, height, width, dtype, false, S(stream));
+}
+int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void* coefs,
+                          void* frames, int32_t nframes, int32_t height, int32_t width,
+                          int32_t dtype, void* stream) {
+  return run_frames(h, v, coefs, frames, nframes, height, width, dtype, true, S(stream));
+}
+
+const char* dctadj_status_string(int32_t status) {
+  switch (status) {
+    case DCTADJ_OK: return "ok";
+    case DCTADJ_ERR_DIMENSION: return "InvalidDimensionError";
+    case DCTADJ_ERR_SHAPE: return "ShapeError";
+    case DCTADJ_ERR_PATTERN: return "PatternError";
+    case DCTADJ_ERR_CONFIG: return "ConfigurationError";
+    case DCTADJ_ERR_KIND: return "KindMismatchError";
+    case DCTADJ_ERR_CUDA: return "CudaError";
+    case DCTADJ_ERR_UNSUPPORTED: return "Unsupported";
+    case DCTADJ_ERR_VALUE: return "ValueError";
+    default: return "unknown";
+  }
+}
+const char* dctadj_last_error(void) { return g_err; }
+int32_t dctadj_version(void) { return 1; }
+int32_t dctadj_kernel_count(void) {
+  return static_cast<int32_t>(sizeof(kRegistry) / sizeof(kRegistry[0]));
+}
+
+}  // extern "C"

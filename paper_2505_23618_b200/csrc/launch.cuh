@@ -1,0 +1,143 @@
+// launch.cuh -- host-side launcher for one tile_kernel instantiation:
+// builds the TMA tensor maps, packs the per-axis coefficients into the kernel
+// parameter block (they are read as constant-bank operands by the FMAs), sizes
+// a persistent grid, and launches on the caller's stream.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "tile_kernel.cuh"
+
+namespace dctadj {
+
+enum DType : int { DT_F32 = 0, DT_F64 = 1 };
+
+struct LaunchArgs {
+  const void* in = nullptr;
+  void* out = nullptr;
+  // LINEAR side: total rows (nblk * H for 2-D, nvec for 1-D)
+  int64_t rows = 0;
+  // FRAME side: nframes x frame_h x frame_w samples
+  int32_t frames = 0, frame_h = 0, frame_w = 0;
+  const void* row_coef = nullptr;  // host, packed AxisOp::Coef of the row op
+  const void* col_coef = nullptr;  // host, packed AxisOp::Coef of the column op
+  const void* dense_row = nullptr; // device, W x W (row op ST_DENSE)
+  const void* dense_col = nullptr; // device, H x H (column op ST_DENSE)
+  cudaStream_t stream = nullptr;
+};
+
+// status codes shared with the C-ABI (include/dctadj.h)
+enum : int {
+  ST_OK = 0,
+  ST_ERR_DIMENSION = 1,
+  ST_ERR_SHAPE = 2,
+  ST_ERR_PATTERN = 3,
+  ST_ERR_CONFIG = 4,
+  ST_ERR_KIND = 5,
+  ST_ERR_CUDA = 6,
+  ST_ERR_UNSUPPORTED = 7,
+  ST_ERR_VALUE = 8,
+};
+
+// implemented in abi.cu
+int encode_tensor_map(CUtensorMap* map, int dtype, int rank, const uint64_t* dims,
+                      const uint64_t* strides_bytes, const uint32_t* box, int box_row_bytes,
+                      void* base);
+int num_sms_cached();
+void set_last_error(const char* fmt, ...);
+
+template <typename T, int H, int W, int P, int MODE>
+int make_map(CUtensorMap* map, const void* base, const LaunchArgs& a) {
+  using L = TileLayout<T, H, W, P>;
+  constexpr int dt = sizeof(T) == 4 ? DT_F32 : DT_F64;
+  if constexpr (MODE == MODE_LINEAR) {
+    uint64_t dims[2] = {static_cast<uint64_t>(W), static_cast<uint64_t>(a.rows)};
+    uint64_t strides[1] = {static_cast<uint64_t>(W) * sizeof(T)};
+    uint32_t box[2] = {static_cast<uint32_t>(L::BW), static_cast<uint32_t>(L::PH)};
+    return encode_tensor_map(map, dt, 2, dims, strides, box, L::BRB, const_cast<void*>(base));
+  } else {
+    uint64_t dims[3] = {static_cast<uint64_t>(a.frame_w), static_cast<uint64_t>(a.frame_h),
+                        static_cast<uint64_t>(a.frames)};
+    uint64_t strides[2] = {static_cast<uint64_t>(a.frame_w) * sizeof(T),
+                           static_cast<uint64_t>(a.frame_w) * a.frame_h * sizeof(T)};
+    uint32_t box[3] = {static_cast<uint32_t>(L::BW), static_cast<uint32_t>(H), 1u};
+    return encode_tensor_map(map, dt, 3, dims, strides, box, L::BRB, const_cast<void*>(base));
+  }
+}
+
+template <typename T, int H, int W, int P, int RC, int CC, bool COL_FIRST, int IN_MODE,
+          int OUT_MODE, int NG, int S>
+int launch_tile(const LaunchArgs& a) {
+  using L = TileLayout<T, H, W, P>;
+  using RowOp = AxisOp<T, W, RC>;
+  using ColOp = AxisOp<T, H, CC>;
+  static_assert(S >= 2, "ring needs at least two stages");
+  static_assert(IN_MODE == MODE_LINEAR || P == 1, "frame tiles are single blocks");
+  static_assert(OUT_MODE == MODE_LINEAR || P == 1, "frame tiles are single blocks");
+
+  Geom g{};
+  if (IN_MODE == MODE_FRAME || OUT_MODE == MODE_FRAME) {
+    g.tiles_y = (a.frame_h + H - 1) / H;
+    g.tiles_x = a.frame_w / W;
+    g.ntiles = static_cast<int64_t>(a.frames) * g.tiles_y * g.tiles_x;
+  } else {
+    g.ntiles = (a.rows + L::PH - 1) / L::PH;
+  }
+  if (g.ntiles == 0) return ST_OK;
+  g.dense_row = a.dense_row;
+  g.dense_col = a.dense_col;
+
+  // the LINEAR side of a frame launch holds ntiles whole blocks
+  LaunchArgs la = a;
+  if (IN_MODE == MODE_FRAME || OUT_MODE == MODE_FRAME) la.rows = g.ntiles * H;
+
+  CUtensorMap in_map, out_map;
+  int rc = make_map<T, H, W, P, IN_MODE>(&in_map, a.in, la);
+  if (rc) return rc;
+  rc = make_map<T, H, W, P, OUT_MODE>(&out_map, a.out, la);
+  if (rc) return rc;
+
+  KParams<T, W, H, RC, CC> prm;
+  std::memset(&prm, 0, sizeof(prm));
+  if (RowOp::NCOEF > 0) std::memcpy(prm.row.c, a.row_coef, sizeof(T) * RowOp::NCOEF);
+  if (ColOp::NCOEF > 0) std::memcpy(prm.col.c, a.col_coef, sizeof(T) * ColOp::NCOEF);
+
+  auto kern = tile_kernel<T, H, W, P, RC, CC, COL_FIRST, IN_MODE, OUT_MODE, NG, S>;
+  const size_t dense_bytes =
+      sizeof(T) * ((RowOp::kDense ? W * W : 0) + (ColOp::kDense ? H * H : 0));
+  const size_t smem = 1024 + static_cast<size_t>(NG) * S * L::STAGEB + NG * S * 8 + dense_bytes;
+
+  static int configured = 0;  // per instantiation
+  static int blocks_per_sm = 1;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      set_last_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+      return ST_ERR_CUDA;
+    }
+    int nb = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NG * 32, smem);
+    if (e != cudaSuccess || nb < 1) {
+      set_last_error("occupancy query failed (%s, %d blocks)", cudaGetErrorString(e), nb);
+      return ST_ERR_CUDA;
+    }
+    blocks_per_sm = nb;
+    configured = 1;
+  }
+  const int64_t want = (g.ntiles + NG - 1) / NG;
+  const int64_t cap = static_cast<int64_t>(num_sms_cached()) * blocks_per_sm;
+  const int grid = static_cast<int>(want < cap ? want : cap);
+
+  kern<<<grid, NG * 32, smem, a.stream>>>(in_map, out_map, g, prm);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_error("tile_kernel launch: %s", cudaGetErrorString(e));
+    return ST_ERR_CUDA;
+  }
+  return ST_OK;
+}
+
+}  // namespace dctadj

@@ -1,0 +1,335 @@
+// tile_kernel.cuh -- the one persistent, TMA-fed tile kernel behind every
+// entry point of the C-ABI.
+//
+// A "super-tile" is P consecutive H x W blocks (P*H rows of W samples).  Each
+// warp owns an S-stage ring of super-tile buffers in shared memory:
+//   TMA 2-D tile load (128B/64B/32B swizzle, zero-filled out of bounds)
+//     -> mbarrier complete_tx
+//     -> row pass: lane r owns row r, 16-byte swizzled LDS into registers,
+//        register butterfly + adjustment, STS back in place
+//     -> column pass: lane c owns column c (conflict-free under the swizzle)
+//     -> fence.proxy.async -> TMA 2-D tile store (clipped out of bounds)
+// The forward transform runs rows then columns (reference pipeline.py:236-239);
+// the inverse runs columns then rows (its mirror).  The 1-D batch API is the
+// same kernel with 32 vectors per tile and no column op.
+//
+// Blocks are independent (reference SPEC.md:313-314), so warps walk the tile
+// list with a static grid stride; HBM traffic is one read and one write per
+// sample.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "butterfly.cuh"
+
+namespace dctadj {
+
+// ---------------------------------------------------------------- PTX helpers
+DA_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+DA_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+DA_DEV void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+DA_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+DA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DA_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra DA_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+DA_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+DA_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                        int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+DA_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+DA_DEV void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+DA_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+DA_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+DA_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+DA_DEV void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+DA_DEV void prefetch_map(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
+}
+
+// ------------------------------------------------------------------ layout
+// Row bytes W*sizeof(T) are cut into boxes of BRB = min(row bytes, 128) bytes;
+// box b of the super-tile occupies BOXB = P*H*BRB contiguous smem bytes with the
+// matching TMA swizzle (128B/64B/32B; none for 16-byte rows).
+template <typename T, int H, int W, int P>
+struct TileLayout {
+  static constexpr int ES = sizeof(T);
+  static constexpr int ROWB = W * ES;
+  static constexpr int BRB = ROWB < 128 ? ROWB : 128;
+  static constexpr int NB = ROWB / BRB;
+  static constexpr int BW = BRB / ES;  // elements per box row
+  static constexpr int PH = P * H;
+  static constexpr int BOXB = PH * BRB;
+  static constexpr int TILEB = NB * BOXB;
+  static constexpr int STAGEB = (TILEB + 1023) / 1024 * 1024;
+  static constexpr int SWZ_MASK = BRB == 128 ? 7 : BRB == 64 ? 3 : BRB == 32 ? 1 : 0;
+  static_assert(BRB >= 16, "rows shorter than 16 bytes are not TMA-addressable");
+  static_assert(PH % 32 == 0, "super-tile rows must cover whole warps");
+  // physical byte offset of (row rho, byte offset `byte` within the row)
+  static DA_DEV uint32_t addr(uint32_t rho, uint32_t byte) {
+    const uint32_t b = byte / BRB, off = byte % BRB;
+    const uint32_t a = rho * BRB + off;
+    return b * BOXB + (a ^ (((a >> 7) & SWZ_MASK) << 4));
+  }
+};
+
+enum Mode : int { MODE_LINEAR = 0, MODE_FRAME = 1 };
+
+struct Geom {
+  int64_t ntiles;      // super-tiles
+  int32_t tiles_y;     // FRAME: tile rows per frame
+  int32_t tiles_x;     // FRAME: tile columns per frame
+  const void* dense_row;  // device N x N (T) for ST_DENSE row op
+  const void* dense_col;  // device N x N (T) for ST_DENSE column op
+};
+
+template <typename T, int W, int H, int RC, int CC>
+struct KParams {
+  typename AxisOp<T, W, RC>::Coef row;
+  typename AxisOp<T, H, CC>::Coef col;
+};
+
+template <typename T, int H, int W, int P, int MODE>
+DA_DEV void issue_tile_io(bool load, void* stage, const CUtensorMap* map, uint64_t* bar,
+                          int64_t t, const Geom& g) {
+  using L = TileLayout<T, H, W, P>;
+#pragma unroll
+  for (int b = 0; b < L::NB; ++b) {
+    uint8_t* dst = static_cast<uint8_t*>(stage) + b * L::BOXB;
+    if constexpr (MODE == MODE_LINEAR) {
+      const int row0 = static_cast<int>(t * L::PH);
+      if (load)
+        tma_load_2d(dst, map, bar, b * L::BW, row0);
+      else
+        tma_store_2d(map, dst, b * L::BW, row0);
+    } else {
+      const int64_t per = static_cast<int64_t>(g.tiles_x) * g.tiles_y;
+      const int f = static_cast<int>(t / per);
+      const int rem = static_cast<int>(t - f * per);
+      const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+      if (load)
+        tma_load_3d(dst, map, bar, tx * W + b * L::BW, ty * H, f);
+      else
+        tma_store_3d(map, dst, tx * W + b * L::BW, ty * H, f);
+    }
+  }
+}
+
+// 1 / (gain_row * gain_col), gains^2 being powers of two: exact unless odd exponent
+__host__ __device__ constexpr double inv_sqrt_pow2(int gsq) {
+  int e = 0;
+  while ((1 << e) < gsq) ++e;
+  double s = 1.0;
+  for (int i = 0; i < e / 2; ++i) s *= 0.5;
+  return (e % 2) ? s * K_SQRT1_2 : s;
+}
+
+template <typename T, int H, int W, int P, int RC, int CC, int GSQ>
+DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Coef& cf,
+                     const T* dense) {
+  using L = TileLayout<T, H, W, P>;
+  constexpr int PER16 = 16 / sizeof(T);
+#pragma unroll 1
+  for (int it = 0; it < L::PH / 32; ++it) {
+    const uint32_t rho = it * 32 + lane;
+    T v[W];
+#pragma unroll
+    for (int q = 0; q < W / PER16; ++q) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(buf + L::addr(rho, q * 16));
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int k = 0; k < PER16; ++k) v[q * PER16 + k] = e[k];
+    }
+    apply_axis<T, W, RC>(v, cf, dense);
+    if constexpr (GSQ > 1) {
+      constexpr T sc = T(inv_sqrt_pow2(GSQ));
+#pragma unroll
+      for (int i = 0; i < W; ++i) v[i] *= sc;
+    }
+#pragma unroll
+    for (int q = 0; q < W / PER16; ++q) {
+      uint4 raw;
+      T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+      for (int k = 0; k < PER16; ++k) e[k] = v[q * PER16 + k];
+      *reinterpret_cast<uint4*>(buf + L::addr(rho, q * 16)) = raw;
+    }
+  }
+}
+
+template <typename T, int H, int W, int P, int RC, int CC, int GSQ>
+DA_DEV void col_pass(uint8_t* buf, int lane, const typename AxisOp<T, H, CC>::Coef& cf,
+                     const T* dense) {
+  using L = TileLayout<T, H, W, P>;
+#pragma unroll 1
+  for (int it = 0; it < (P * W) / 32; ++it) {
+    const int kappa = it * 32 + lane;
+    const uint32_t p = kappa / W, c = kappa % W;
+    const uint32_t byte = c * sizeof(T);
+    T v[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) v[i] = *reinterpret_cast<const T*>(buf + L::addr(p * H + i, byte));
+    apply_axis<T, H, CC>(v, cf, dense);
+    if constexpr (GSQ > 1) {
+      constexpr T sc = T(inv_sqrt_pow2(GSQ));
+#pragma unroll
+      for (int i = 0; i < H; ++i) v[i] *= sc;
+    }
+#pragma unroll
+    for (int i = 0; i < H; ++i) *reinterpret_cast<T*>(buf + L::addr(p * H + i, byte)) = v[i];
+  }
+}
+
+// NG warps per CTA, each with an S-stage ring.
+template <typename T, int H, int W, int P, int RC, int CC, bool COL_FIRST, int IN_MODE,
+          int OUT_MODE, int NG, int S>
+__global__ void __launch_bounds__(NG * 32)
+    tile_kernel(const __grid_constant__ CUtensorMap in_map,
+                const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
+                const __grid_constant__ KParams<T, W, H, RC, CC> prm) {
+  using L = TileLayout<T, H, W, P>;
+  using RowOp = AxisOp<T, W, RC>;
+  using ColOp = AxisOp<T, H, CC>;
+  static_assert(ColOp::kIdentity || (P * W) % 32 == 0, "column pass must cover whole warps");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // dynamic smem is only guaranteed 16-byte aligned: round up to 1024 for the swizzle atom
+  // (pointer arithmetic, not an integer round trip, keeps the shared address space)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * S * L::STAGEB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NG * S * L::STAGEB) + warp * S;
+  T* dense_base = reinterpret_cast<T*>(smem + NG * S * L::STAGEB + NG * S * 8);
+  T* dense_row = dense_base;
+  T* dense_col = dense_base + (RowOp::kDense ? W * W : 0);
+
+  if constexpr (RowOp::kDense || ColOp::kDense) {
+    if constexpr (RowOp::kDense) {
+      const T* src = static_cast<const T*>(geom.dense_row);
+      for (int i = threadIdx.x; i < W * W; i += NG * 32) dense_row[i] = src[i];
+    }
+    if constexpr (ColOp::kDense) {
+      const T* src = static_cast<const T*>(geom.dense_col);
+      for (int i = threadIdx.x; i < H * H; i += NG * 32) dense_col[i] = src[i];
+    }
+    __syncthreads();
+  }
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    if (warp == 0) {
+      prefetch_map(&in_map);
+      prefetch_map(&out_map);
+    }
+  }
+  __syncwarp();
+
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * NG + warp;
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * NG;
+  const int64_t ntiles = geom.ntiles;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int64_t t = gid + s * gstride;
+      if (t < ntiles) {
+        mbar_arrive_expect_tx(&bars[s], L::TILEB);
+        issue_tile_io<T, H, W, P, IN_MODE>(true, ring + s * L::STAGEB, &in_map, &bars[s], t, geom);
+      }
+    }
+  }
+
+  int s = 0;
+  uint32_t phase = 0;
+  for (int64_t t = gid, k = 0; t < ntiles; t += gstride, ++k) {
+    uint8_t* buf = ring + s * L::STAGEB;
+    mbar_wait(&bars[s], phase);
+    // the unnormalized base gains of both axes are removed in the last pass
+    constexpr int GSQ = RowOp::kGainSq * ColOp::kGainSq;
+    if constexpr (!COL_FIRST) {
+      if constexpr (!RowOp::kIdentity) {
+        row_pass<T, H, W, P, RC, CC, ColOp::kIdentity ? GSQ : 1>(buf, lane, prm.row, dense_row);
+        if constexpr (!ColOp::kIdentity) __syncwarp();
+      }
+      if constexpr (!ColOp::kIdentity)
+        col_pass<T, H, W, P, RC, CC, GSQ>(buf, lane, prm.col, dense_col);
+    } else {
+      if constexpr (!ColOp::kIdentity) {
+        col_pass<T, H, W, P, RC, CC, RowOp::kIdentity ? GSQ : 1>(buf, lane, prm.col, dense_col);
+        if constexpr (!RowOp::kIdentity) __syncwarp();
+      }
+      if constexpr (!RowOp::kIdentity)
+        row_pass<T, H, W, P, RC, CC, GSQ>(buf, lane, prm.row, dense_row);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      issue_tile_io<T, H, W, P, OUT_MODE>(false, buf, &out_map, nullptr, t, geom);
+      bulk_commit();
+      // refill the stage freed by the previous tile with the tile S-1 strides ahead
+      if (k >= 1) {
+        const int64_t tn = t + (S - 1) * gstride;
+        if (tn < ntiles) {
+          const int sp = (s == 0) ? S - 1 : s - 1;
+          bulk_wait_read<1>();
+          mbar_arrive_expect_tx(&bars[sp], L::TILEB);
+          issue_tile_io<T, H, W, P, IN_MODE>(true, ring + sp * L::STAGEB, &in_map, &bars[sp], tn,
+                                             geom);
+        }
+      }
+    }
+    __syncwarp();
+    if (++s == S) {
+      s = 0;
+      phase ^= 1;
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
+}  // namespace dctadj

@@ -1,0 +1,279 @@
+"""Adjusted-transform pipelines: the reference's drop-in entry points plus the
+fused 2-D / frame entries of the B200 build.
+
+Reference names and semantics kept (reference pkg/src/dctadjust/pipeline.py):
+  FAST_SIZES, BasePath                                   :32-37
+  fast_dct2 / fast_idct2 / fast_dst3_via_dct2 / fast_idst3 :64-87
+  apply_band / apply_subblock                            :90-108
+  AdjustedTransform / make_adjusted_transform            :127-155
+  forward_adjusted / inverse_adjusted                    :176-191
+  dense_matrix                                           :194-199
+Each call is ONE fused kernel (adjustment + butterfly, no intermediate HBM
+round trip) behind the C-ABI.  New entries:
+  forward_adjusted_2d / inverse_adjusted_2d   (nblk, H, W) blocks, rows then
+                                              columns (the order of _dct2_2d,
+                                              pipeline.py:236-239), one kernel
+  forward_frames / inverse_frames             whole frames tiled into blocks
+  forward_adjusted_2d_host / ..._host         host buffers, pipelined copies
+Extension: base DCT-3 is accepted (the DCT-8 pre-adjustment, SURVEY.md App. A
+D3, built with design.flip_pre_adjustment); the reference raises
+ConfigurationError for it.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from . import _device, _lib, kernels
+from .design import AdjustmentMatrix, PatternKind, Side
+from .errors import ConfigurationError, InvalidDimensionError, PatternError, ShapeError
+from .transforms import TransformKind, build_transform
+
+FAST_SIZES = (4, 8, 16, 32, 64)
+
+
+class BasePath(Enum):
+    FAST_DCT2 = "fast_dct2"
+    FAST_DST3_VIA_DCT2 = "fast_dst3_via_dct2"
+    FAST_DCT3 = "fast_dct3"  # extension: DCT-8 pre flip (App. A D3)
+
+
+_BASE_CODE = {BasePath.FAST_DCT2: _lib.BASE_DCT2, BasePath.FAST_DST3_VIA_DCT2: _lib.BASE_DST3,
+              BasePath.FAST_DCT3: _lib.BASE_DCT3}
+_ADJ_CODE = {PatternKind.BAND: _lib.ADJ_BAND, PatternKind.SUBBLOCK: _lib.ADJ_SUBBLOCK,
+             PatternKind.DENSE: _lib.ADJ_DENSE}
+
+
+def _check_fast_size(n: int) -> None:
+    if n not in FAST_SIZES:
+        raise InvalidDimensionError(f"fast transforms support sizes {FAST_SIZES}, got {n}")
+
+
+def _width(x) -> int:
+    shape = tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
+    return shape[-1] if shape else 0
+
+
+def _as_batch(x, n: int):
+    """(contiguous device batch (nvec, n), was_vector, returns_numpy)."""
+    t, as_np = _device.to_device(x)
+    if t.dim() == 1:
+        if t.shape[0] != n:
+            raise ShapeError(f"vector length {t.shape[0]}, expected {n}")
+        return t.reshape(1, n), True, as_np
+    if t.dim() == 2:
+        if t.shape[1] != n:
+            raise ShapeError(f"batch width {t.shape[1]}, expected {n}")
+        return t, False, as_np
+    raise ShapeError(f"expected a vector or batch of vectors, got ndim={t.dim()}")
+
+
+def _debatch(t, was_vector: bool, as_np: bool):
+    out = _device.from_device(t, as_np)
+    return out[0] if was_vector else out
+
+
+def _fast(fn, x):
+    n = _width(x)
+    _check_fast_size(n)
+    t, single, as_np = _as_batch(x, n)
+    y = _device.empty_like(t)
+    _lib.call(fn, t.data_ptr(), y.data_ptr(), t.shape[0], n, _device.dtype_code(t),
+              _device.stream_handle())
+    return _debatch(y, single, as_np)
+
+
+def fast_dct2(x):
+    """Orthonormal DCT-2 through the fast butterfly."""
+    return _fast("dctadj_dct2", x)
+
+
+def fast_idct2(y):
+    return _fast("dctadj_idct2", y)
+
+
+def fast_dst3_via_dct2(x):
+    """DST-3 at DCT-2 cost: reversal + inverse fast DCT-2 + sign flips."""
+    return _fast("dctadj_dst3", x)
+
+
+def fast_idst3(y):
+    return _fast("dctadj_idst3", y)
+
+
+def apply_band(adj: AdjustmentMatrix, x):
+    """y = A x for a band adjustment (only the K-tap window of each row)."""
+    if adj.pattern.kind is not PatternKind.BAND:
+        raise PatternError(f"apply_band needs a band adjustment, got {adj.pattern.label()}")
+    t, single, as_np = _as_batch(x, adj.pattern.size)
+    return _debatch(kernels.band(adj.realized, adj.pattern.taps, t), single, as_np)
+
+
+def apply_subblock(adj: AdjustmentMatrix, y):
+    """Leading B coefficients times the block; the rest bit-identical."""
+    if adj.pattern.kind is not PatternKind.SUBBLOCK:
+        raise PatternError(
+            f"apply_subblock needs a sub-block adjustment, got {adj.pattern.label()}")
+    t, single, as_np = _as_batch(y, adj.pattern.size)
+    b = adj.pattern.order
+    return _debatch(kernels.subblock(adj.realized[:b, :b], t), single, as_np)
+
+
+@dataclass(frozen=True)
+class AdjustedTransform:
+    """A runnable approximation of DST-7 or DCT-8: adjustment + fast base."""
+
+    target: TransformKind
+    size: int
+    adjustment: AdjustmentMatrix
+    base_path: BasePath
+
+    def axis(self) -> tuple[_lib.Axis, np.ndarray]:
+        """The C-ABI descriptor (and the matrix buffer it points into)."""
+        adj = self.adjustment
+        mat = np.ascontiguousarray(adj.realized, dtype=np.float64)
+        ax = _lib.Axis(self.size, _BASE_CODE[self.base_path], _ADJ_CODE[adj.pattern.kind],
+                       _lib.SIDE_PRE if adj.side is Side.PRE else _lib.SIDE_POST,
+                       adj.pattern.taps or 0, adj.pattern.order or 0, _lib.dptr(mat))
+        return ax, mat
+
+
+def make_adjusted_transform(adj: AdjustmentMatrix) -> AdjustedTransform:
+    """Bind an adjustment to its fast base (DST-3 for pre, DCT-2 for post)."""
+    _check_fast_size(adj.pattern.size)
+    if adj.base is TransformKind.DCT2:
+        path = BasePath.FAST_DCT2
+    elif adj.base is TransformKind.DST3:
+        path = BasePath.FAST_DST3_VIA_DCT2
+    elif adj.base is TransformKind.DCT3:
+        path = BasePath.FAST_DCT3
+    else:
+        raise ConfigurationError(
+            f"no fast path for base transform {adj.base}; use dct2, dst3 or dct3")
+    return AdjustedTransform(adj.target, adj.pattern.size, adj, path)
+
+
+def _run_1d(fn: str, t: AdjustedTransform, x):
+    arr, single, as_np = _as_batch(x, t.size)
+    y = _device.empty_like(arr)
+    ax, _keep = t.axis()
+    _lib.call(fn, ctypes.byref(ax), arr.data_ptr(), y.data_ptr(), arr.shape[0],
+              _device.dtype_code(arr), _device.stream_handle())
+    return _debatch(y, single, as_np)
+
+
+def forward_adjusted(t: AdjustedTransform, x):
+    """PRE: y = B(A x);  POST: y = C(B x) -- one fused kernel."""
+    return _run_1d("dctadj_forward_1d", t, x)
+
+
+def inverse_adjusted(t: AdjustedTransform, y):
+    """PRE: x = A^T(B^-1 y);  POST: x = B^-1(C^T y) -- one fused kernel."""
+    return _run_1d("dctadj_inverse_1d", t, y)
+
+
+def dense_matrix(t: AdjustedTransform) -> np.ndarray:
+    """The exact H this pipeline realizes (oracle / comparison path)."""
+    base = build_transform(t.adjustment.base, t.size).entries
+    a = t.adjustment.realized
+    return base @ a if t.adjustment.side is Side.PRE else a @ base
+
+
+# ---------------------------------------------------------------- 2-D blocks
+def _as_blocks(x, h: int, w: int):
+    t, as_np = _device.to_device(x)
+    if t.dim() == 2:
+        if tuple(t.shape) != (h, w):
+            raise ShapeError(f"block {tuple(t.shape)}, expected ({h}, {w})")
+        return t.reshape(1, h, w), True, as_np
+    if t.dim() == 3:
+        if tuple(t.shape[1:]) != (h, w):
+            raise ShapeError(f"blocks {tuple(t.shape[1:])}, expected ({h}, {w})")
+        return t, False, as_np
+    raise ShapeError(f"expected (H, W) or (nblk, H, W) blocks, got ndim={t.dim()}")
+
+
+def _run_2d(fn: str, th: AdjustedTransform, tv: AdjustedTransform, x):
+    blk, single, as_np = _as_blocks(x, tv.size, th.size)
+    y = _device.empty_like(blk)
+    (axh, _kh), (axv, _kv) = th.axis(), tv.axis()
+    _lib.call(fn, ctypes.byref(axh), ctypes.byref(axv), blk.data_ptr(), y.data_ptr(),
+              blk.shape[0], _device.dtype_code(blk), _device.stream_handle())
+    return _debatch(y, single, as_np)
+
+
+def forward_adjusted_2d(th: AdjustedTransform, tv: AdjustedTransform, x):
+    """Y = T_v X T_h^T per (H, W) block: rows with th (length W), then columns
+    with tv (length H), fused in one kernel."""
+    return _run_2d("dctadj_forward_2d", th, tv, x)
+
+
+def inverse_adjusted_2d(th: AdjustedTransform, tv: AdjustedTransform, y):
+    """X = T_v^T Y T_h: columns, then rows (the mirror of the forward)."""
+    return _run_2d("dctadj_inverse_2d", th, tv, y)
+
+
+def _run_2d_host(fn: str, th: AdjustedTransform, tv: AdjustedTransform, x, out=None):
+    arr = np.asarray(x)
+    if arr.dtype not in (np.float32, np.float64):
+        arr = arr.astype(np.float64)
+    arr = np.ascontiguousarray(arr)
+    if arr.ndim != 3 or arr.shape[1:] != (tv.size, th.size):
+        raise ShapeError(f"expected (nblk, {tv.size}, {th.size}) blocks, got {arr.shape}")
+    y = np.empty_like(arr) if out is None else out
+    (axh, _kh), (axv, _kv) = th.axis(), tv.axis()
+    _device.require_cuda()
+    _lib.call(fn, ctypes.byref(axh), ctypes.byref(axv), arr.ctypes.data, y.ctypes.data,
+              arr.shape[0], _lib.F32 if arr.dtype == np.float32 else _lib.F64,
+              _device.torch.cuda.current_device())
+    return y
+
+
+def forward_adjusted_2d_host(th, tv, x, out=None):
+    """forward_adjusted_2d on host arrays (pinned for full speed); the copies
+    and kernels are pipelined inside the library."""
+    return _run_2d_host("dctadj_forward_2d_host", th, tv, x, out)
+
+
+def inverse_adjusted_2d_host(th, tv, y, out=None):
+    return _run_2d_host("dctadj_inverse_2d_host", th, tv, y, out)
+
+
+# ---------------------------------------------------------------- frames
+def frame_block_count(nframes: int, height: int, width: int, h: int, w: int) -> int:
+    return nframes * (-(-height // h)) * (width // w)
+
+
+def forward_frames(th: AdjustedTransform, tv: AdjustedTransform, frames):
+    """(F, height, width) frames -> block-major coefficients (nblk, H, W), blocks
+    in raster order per frame; rows past `height` are zero padding."""
+    t, as_np = _device.to_device(frames)
+    if t.dim() != 3:
+        raise ShapeError(f"expected (F, height, width) frames, got ndim={t.dim()}")
+    f, hh, ww = t.shape
+    nblk = frame_block_count(f, hh, ww, tv.size, th.size)
+    y = _device.empty_like(t, (nblk, tv.size, th.size))
+    (axh, _kh), (axv, _kv) = th.axis(), tv.axis()
+    _lib.call("dctadj_forward_frames", ctypes.byref(axh), ctypes.byref(axv), t.data_ptr(),
+              y.data_ptr(), f, hh, ww, _device.dtype_code(t), _device.stream_handle())
+    return _device.from_device(y, as_np)
+
+
+def inverse_frames(th: AdjustedTransform, tv: AdjustedTransform, coefs, height: int,
+                   width: int):
+    """Block-major coefficients -> (F, height, width) frames (padding clipped)."""
+    t, as_np = _device.to_device(coefs)
+    if t.dim() != 3 or tuple(t.shape[1:]) != (tv.size, th.size):
+        raise ShapeError(f"expected (nblk, {tv.size}, {th.size}) coefficients")
+    per = frame_block_count(1, height, width, tv.size, th.size)
+    if per == 0 or t.shape[0] % per:
+        raise ShapeError(f"{t.shape[0]} blocks do not tile frames of {height} x {width}")
+    f = t.shape[0] // per
+    y = _device.empty_like(t, (f, height, width))
+    (axh, _kh), (axv, _kv) = th.axis(), tv.axis()
+    _lib.call("dctadj_inverse_frames", ctypes.byref(axh), ctypes.byref(axv), t.data_ptr(),
+              y.data_ptr(), f, height, width, _device.dtype_code(t), _device.stream_handle())
+    return _device.from_device(y, as_np)

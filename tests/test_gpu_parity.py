@@ -1,0 +1,336 @@
+"""GPU parity: every entry point of the C-ABI (through the Python mirror) against
+the CPU oracle and the reference's golden vectors.
+
+Tolerances (BASELINE.json north_star): per-block normwise
+relative error <= 1e-9 for fp64, <= 1e-5 for fp32.  Bit-exact checks: the
+sub-block tail equals the build's own base output, the identity adjustment
+equals the base, and rint(inverse(forward(x))) == x for integer residuals.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import rel_err  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from paper_2505_23618_b200 import kernels, matio, pipeline  # noqa: E402
+from paper_2505_23618_b200.design import (SparsityPattern, Side, dct8_adjustment_from_dst7,  # noqa: E402
+                                          flip_pre_adjustment, identity_adjustment,
+                                          random_adjustment)
+from paper_2505_23618_b200.errors import (InvalidDimensionError, PatternError,  # noqa: E402
+                                          ShapeError, ConfigurationError)
+from paper_2505_23618_b200.transforms import TransformKind, build_transform  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+F64_TOL = 1e-9
+F32_TOL = 1e-5
+
+
+def oaxis(adj):
+    base = {"dct2": O.BASE_DCT2, "dst3": O.BASE_DST3, "dct3": O.BASE_DCT3}[adj.base.value]
+    kind = {"band": O.ADJ_BAND, "subblock": O.ADJ_SUBBLOCK, "dense": O.ADJ_DENSE}[adj.pattern.kind.value]
+    return O.OAxis(adj.pattern.size, base, kind, O.SIDE_PRE if adj.side is Side.PRE else O.SIDE_POST,
+                   adj.pattern.taps or 0, adj.pattern.order or 0, np.array(adj.realized))
+
+
+def dev(x, dtype=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+# ---------------------------------------------------------------- primitives
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64])
+@pytest.mark.parametrize("fn", ["dct2", "idct2", "dst3", "idst3"])
+def test_primitives_fp64_numpy(golden, n, fn):
+    x = golden[f"prim/x/{n}"]
+    got = getattr(kernels, fn)(x)
+    assert isinstance(got, np.ndarray) and got.dtype == np.float64
+    assert rel_err(got, golden[f"prim/{fn}/{n}"]) < F64_TOL
+
+
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64])
+@pytest.mark.parametrize("fn", ["dct2", "idct2", "dst3", "idst3"])
+def test_primitives_fp32_tensor(golden, n, fn):
+    x = golden[f"prim/x/{n}"]
+    got = getattr(kernels, fn)(dev(x))
+    assert got.dtype == torch.float32 and got.is_cuda
+    assert rel_err(got.cpu().numpy(), golden[f"prim/{fn}/{n}"]) < F32_TOL
+
+
+@pytest.mark.parametrize("n", [4, 8, 16, 32, 64])
+def test_band_subblock_dense(golden, n):
+    x = golden[f"prim/x/{n}"]
+    for taps in (3, 4, 6):
+        key = f"prim/band/{n}/{taps}"
+        if key in golden:
+            a = golden[f"prim/band_a/{n}/{taps}"]
+            assert rel_err(kernels.band(a, taps, x), golden[key]) < F64_TOL
+            assert rel_err(kernels.band(a, taps, dev(x)).cpu().numpy(), golden[key]) < F32_TOL
+    for b in (5, 8):
+        key = f"prim/sub/{n}/{b}"
+        if key in golden:
+            blk = golden[f"prim/sub_blk/{n}/{b}"]
+            got = kernels.subblock(blk, x)
+            assert rel_err(got, golden[key]) < F64_TOL
+            assert np.array_equal(got[:, b:], x[:, b:])  # tail bit-identical
+            got32 = kernels.subblock(blk, dev(x)).cpu().numpy()
+            assert np.array_equal(got32[:, b:], x[:, b:].astype(np.float32))
+    assert rel_err(kernels.dense(golden[f"prim/dense_m/{n}"], x), golden[f"prim/dense/{n}"]) < F64_TOL
+
+
+def test_dense_rect(golden):
+    got = kernels.dense(golden["prim/dense_rect_m"], golden["prim/dense_rect_x"])
+    assert got.shape == (37, 16)
+    assert rel_err(got, golden["prim/dense_rect"]) < F64_TOL
+
+
+# ---------------------------------------------------------------- 1-D adjusted
+ONE_D = ["band6_pre_dst3_dst7_n16", "band6_pre_dst3_dst7_n32", "band6_pre_dst3_dst7_n64",
+         "band4_pre_dst3_dst7_n32", "sub8_post_dct2_dst7_n16", "sub8_post_dct2_dst7_n32",
+         "sub8_post_dct2_dst7_n64", "sub8_post_dct2_dct8_n32"]
+
+
+def _design(name):
+    if name == "sub8_post_dct2_dct8_n32":
+        return dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    return matio.load_designed(name)
+
+
+@pytest.mark.parametrize("name", ONE_D)
+def test_adjusted_1d(golden, name):
+    adj = _design(name)
+    t = pipeline.make_adjusted_transform(adj)
+    x = golden[f"adj1d/{name}/x"]
+    assert rel_err(pipeline.forward_adjusted(t, x), golden[f"adj1d/{name}/fwd"]) < F64_TOL
+    assert rel_err(pipeline.inverse_adjusted(t, x), golden[f"adj1d/{name}/inv"]) < F64_TOL
+    y32 = pipeline.forward_adjusted(t, dev(x)).cpu().numpy()
+    assert rel_err(y32, golden[f"adj1d/{name}/fwd"]) < F32_TOL
+    if "pre" in name:
+        tf = pipeline.make_adjusted_transform(flip_pre_adjustment(adj))
+        assert rel_err(pipeline.forward_adjusted(tf, x), golden[f"adj1d/{name}/fwd_flip"]) < F64_TOL
+        assert rel_err(pipeline.inverse_adjusted(tf, x), golden[f"adj1d/{name}/inv_flip"]) < F64_TOL
+
+
+def test_vector_input_and_roundtrip():
+    t = pipeline.make_adjusted_transform(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    x = np.random.default_rng(1).standard_normal(32)
+    y = pipeline.forward_adjusted(t, x)
+    assert y.shape == (32,)
+    assert np.abs(y - pipeline.dense_matrix(t) @ x).max() < 1e-9
+    assert np.abs(pipeline.inverse_adjusted(t, y) - x).max() < 1e-9
+
+
+@pytest.mark.parametrize("size", [16, 32, 64])
+@pytest.mark.parametrize("kind", ["band", "subblock"])
+def test_random_adjustments_match_dense(size, kind):
+    # reference test_pipeline.py:161-176 with random-angle schedules
+    if kind == "band":
+        adj = random_adjustment(SparsityPattern.band(6, size), Side.PRE, TransformKind.DST3, 3)
+    else:
+        adj = random_adjustment(SparsityPattern.subblock(8, size), Side.POST, TransformKind.DCT2, 3)
+    t = pipeline.make_adjusted_transform(adj)
+    x = np.random.default_rng(size).standard_normal((50, size))
+    y = pipeline.forward_adjusted(t, x)
+    assert np.abs(y - x @ pipeline.dense_matrix(t).T).max() < 1e-9
+    assert np.abs(pipeline.inverse_adjusted(t, y) - x).max() < 1e-9
+
+
+@pytest.mark.parametrize("taps,order", [(3, None), (5, None), (None, 4), (None, 16)])
+def test_generic_patterns_dense_composite(taps, order):
+    """Widths without a specialised kernel run as a fused dense composite."""
+    n = 32
+    if taps:
+        adj = random_adjustment(SparsityPattern.band(taps, n), Side.PRE, TransformKind.DST3, 7)
+    else:
+        adj = random_adjustment(SparsityPattern.subblock(order, n), Side.POST, TransformKind.DCT2, 7)
+    t = pipeline.make_adjusted_transform(adj)
+    x = np.random.default_rng(2).standard_normal((40, n))
+    assert np.abs(pipeline.forward_adjusted(t, x) - x @ pipeline.dense_matrix(t).T).max() < 1e-9
+
+
+def test_identity_adjustment_equals_base_bitwise():
+    adj = identity_adjustment(SparsityPattern.band(6, 32), Side.PRE, TransformKind.DST3,
+                              TransformKind.DST7)
+    t = pipeline.make_adjusted_transform(adj)
+    x = np.random.default_rng(3).standard_normal((70, 32))
+    assert np.array_equal(pipeline.forward_adjusted(t, x), pipeline.fast_dst3_via_dct2(x))
+    xd = dev(x)
+    assert torch.equal(pipeline.forward_adjusted(t, xd), pipeline.fast_dst3_via_dct2(xd))
+
+
+def test_subblock_tail_equals_own_dct2_bitwise():
+    adj = random_adjustment(SparsityPattern.subblock(8, 32), Side.POST, TransformKind.DCT2, 4)
+    t = pipeline.make_adjusted_transform(adj)
+    x = dev(np.random.default_rng(4).standard_normal((100, 32)))
+    y = pipeline.forward_adjusted(t, x)
+    assert torch.equal(y[:, 8:], pipeline.fast_dct2(x)[:, 8:])
+
+
+def test_zero_and_constant():
+    z = np.zeros((5, 16))
+    assert np.array_equal(pipeline.fast_dct2(z), z)
+    y = pipeline.fast_dct2(np.full((1, 16), 1.7))
+    assert abs(y[0, 0] - 1.7 * 4.0) < 1e-10 and np.abs(y[0, 1:]).max() < 1e-10
+
+
+def test_linearity():
+    t = pipeline.make_adjusted_transform(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    rng = np.random.default_rng(9)
+    x1, x2 = rng.standard_normal(32), rng.standard_normal(32)
+    lhs = pipeline.forward_adjusted(t, 2.5 * x1 - 0.7 * x2)
+    rhs = 2.5 * pipeline.forward_adjusted(t, x1) - 0.7 * pipeline.forward_adjusted(t, x2)
+    assert np.abs(lhs - rhs).max() < 1e-9
+
+
+# ---------------------------------------------------------------- errors / edges
+def test_errors_match_reference_classes():
+    with pytest.raises(InvalidDimensionError):
+        pipeline.fast_dct2(np.zeros((2, 12)))
+    with pytest.raises(InvalidDimensionError):
+        pipeline.fast_dct2(np.zeros((2, 128)))
+    t = pipeline.make_adjusted_transform(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    with pytest.raises(ShapeError):
+        pipeline.forward_adjusted(t, np.zeros(16))
+    with pytest.raises(ShapeError):
+        pipeline.forward_adjusted(t, np.zeros((2, 2, 32)))
+    band = matio.load_designed("band6_pre_dst3_dst7_n32")
+    with pytest.raises(PatternError):
+        pipeline.apply_subblock(band, np.zeros(32))
+    with pytest.raises(PatternError):
+        pipeline.apply_band(matio.load_designed("sub8_post_dct2_dst7_n32"), np.zeros(32))
+    bad = identity_adjustment(SparsityPattern.band(4, 16), Side.PRE, TransformKind.DST2,
+                              TransformKind.DST7)
+    with pytest.raises(ConfigurationError):
+        pipeline.make_adjusted_transform(bad)
+
+
+@pytest.mark.parametrize("nvec", [0, 1, 31, 33, 1000])
+def test_ragged_and_empty_batches(nvec):
+    x = np.random.default_rng(nvec).standard_normal((nvec, 32))
+    y = kernels.dst3(x)
+    assert y.shape == (nvec, 32)
+    if nvec:
+        assert np.abs(y - O.dst3(x)).max() < 1e-12
+
+
+def test_readonly_input_accepted():
+    x = np.random.default_rng(0).standard_normal((4, 16))
+    x.setflags(write=False)
+    kernels.dct2(x)
+
+
+# ---------------------------------------------------------------- 2-D configs
+def test_c1_forward_fp64(golden):
+    t = pipeline.make_adjusted_transform(matio.load_designed("band6_pre_dst3_dst7_n32"))
+    y = pipeline.forward_adjusted_2d(t, t, dev(golden["c1/x"], torch.float64))
+    assert rel_err(y.cpu().numpy(), golden["c1/y"]) < F64_TOL
+
+
+def test_c2_roundtrip_fp32_integer(golden):
+    t = pipeline.make_adjusted_transform(
+        dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32")))
+    x = dev(golden["c2/x"])
+    y = pipeline.forward_adjusted_2d(t, t, x)
+    assert rel_err(y.cpu().numpy(), golden["c2/y"]) < F32_TOL
+    xr = pipeline.inverse_adjusted_2d(t, t, y)
+    assert rel_err(xr.cpu().numpy(), golden["c2/x"]) < F32_TOL
+    assert torch.equal(torch.round(xr), x)  # bit-exact integer recovery (D7 iii)
+
+
+def test_c2_host_entry(golden):
+    t = pipeline.make_adjusted_transform(
+        dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32")))
+    x = np.ascontiguousarray(golden["c2/x"])
+    y = pipeline.forward_adjusted_2d_host(t, t, x)
+    assert y.dtype == np.float32
+    assert rel_err(y, golden["c2/y"]) < F32_TOL
+    xr = pipeline.inverse_adjusted_2d_host(t, t, y)
+    assert np.array_equal(np.rint(xr), x)
+
+
+@pytest.mark.parametrize("tag", ["dst7_pre", "dct8_pre", "dst7_post", "dct8_post"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_c4_n64_variants(golden, tag, dtype):
+    b6 = matio.load_designed("band6_pre_dst3_dst7_n64")
+    s7 = matio.load_designed("sub8_post_dct2_dst7_n64")
+    adj = {"dst7_pre": b6, "dct8_pre": flip_pre_adjustment(b6), "dst7_post": s7,
+           "dct8_post": dct8_adjustment_from_dst7(s7)}[tag]
+    t = pipeline.make_adjusted_transform(adj)
+    tol = F32_TOL if dtype == torch.float32 else F64_TOL
+    x = dev(golden["c4/x"], dtype)
+    assert rel_err(pipeline.forward_adjusted_2d(t, t, x).cpu().numpy(), golden[f"c4/{tag}/y"]) < tol
+    assert rel_err(pipeline.inverse_adjusted_2d(t, t, x).cpu().numpy(), golden[f"c4/{tag}/xr"]) < tol
+
+
+@pytest.mark.parametrize("shape", [(16, 16), (16, 32), (32, 16), (32, 32)])
+@pytest.mark.parametrize("side", ["pre", "post"])
+def test_c3_shapes_and_pairs(golden, shape, side):
+    h, w = shape
+    pre = {n: matio.load_designed(f"band6_pre_dst3_dst7_n{n}") for n in (16, 32)}
+    post = {n: matio.load_designed(f"sub8_post_dct2_dst7_n{n}") for n in (16, 32)}
+
+    def adj(n, kind):
+        if side == "pre":
+            return pre[n] if kind == "dst7" else flip_pre_adjustment(pre[n])
+        return post[n] if kind == "dst7" else dct8_adjustment_from_dst7(post[n])
+
+    x = dev(golden[f"c3/{h}x{w}/x"])
+    for kh in ("dst7", "dct8"):
+        for kv in ("dst7", "dct8"):
+            th = pipeline.make_adjusted_transform(adj(w, kh))
+            tv = pipeline.make_adjusted_transform(adj(h, kv))
+            k = f"c3/{h}x{w}/{side}/{kh}_{kv}"
+            assert rel_err(pipeline.forward_adjusted_2d(th, tv, x).cpu().numpy(), golden[k + "/y"]) < F32_TOL
+            assert rel_err(pipeline.inverse_adjusted_2d(th, tv, x).cpu().numpy(), golden[k + "/xr"]) < F32_TOL
+
+
+def test_c5_frames(golden):
+    t = pipeline.make_adjusted_transform(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    frames = dev(golden["c5/frames"])
+    y = pipeline.forward_frames(t, t, frames)
+    assert tuple(y.shape) == (12, 32, 32)
+    assert rel_err(y.cpu().numpy(), golden["c5/y"]) < F32_TOL
+    back = pipeline.inverse_frames(t, t, y, 48, 96)
+    assert rel_err(back.cpu().numpy(), golden["c5/frames"]) < F32_TOL
+    # exact dense DST-7 comparison path on the same tiles
+    d7 = build_transform(TransformKind.DST7, 32).entries
+    from paper_2505_23618_b200.design import AdjustmentMatrix, pattern_schedule_template
+    dense = AdjustmentMatrix(SparsityPattern.dense(32), Side.POST, TransformKind.DCT2,
+                             TransformKind.DST7, pattern_schedule_template(SparsityPattern.dense(32)),
+                             d7 @ build_transform(TransformKind.DCT2, 32).entries.T)
+    td = pipeline.make_adjusted_transform(dense)
+    ye = pipeline.forward_frames(td, td, frames)
+    assert rel_err(ye.cpu().numpy(), golden["c5/y_exact"]) < F32_TOL
+
+
+def test_2d_identity_tail_bitwise():
+    """Coefficients outside the first 8 rows/cols of a sub8-post 2-D transform
+    equal the plain 2-D DCT-2 bit for bit (reference test_pipeline.py:235-241)."""
+    adj = random_adjustment(SparsityPattern.subblock(8, 32), Side.POST, TransformKind.DCT2, 5)
+    t = pipeline.make_adjusted_transform(adj)
+    plain = pipeline.make_adjusted_transform(identity_adjustment(
+        SparsityPattern.subblock(8, 32), Side.POST, TransformKind.DCT2, TransformKind.DCT2))
+    x = dev(np.random.default_rng(6).standard_normal((64, 32, 32)))
+    y = pipeline.forward_adjusted_2d(t, t, x)
+    y0 = pipeline.forward_adjusted_2d(plain, plain, x)
+    assert torch.equal(y[:, 8:, 8:], y0[:, 8:, 8:])
+
+
+def test_large_batch_properties():
+    """Full-size style check without the oracle: round trip + linearity on
+    65,536 blocks (config 2's size)."""
+    t = pipeline.make_adjusted_transform(
+        dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32")))
+    g = torch.Generator(device="cuda").manual_seed(2)
+    x = torch.round(torch.randn(65536, 32, 32, device="cuda", generator=g) * 24).clamp_(-512, 511)
+    y = pipeline.forward_adjusted_2d(t, t, x)
+    xr = pipeline.inverse_adjusted_2d(t, t, y)
+    assert torch.equal(torch.round(xr), x)
+    # energy preservation (orthogonal transform)
+    e_in, e_out = (x.double() ** 2).sum().item(), (y.double() ** 2).sum().item()
+    assert abs(e_out / e_in - 1) < 1e-6
+    # spot-check 512 random blocks against the oracle
+    idx = torch.randint(0, 65536, (512,), device="cuda", generator=g)
+    xs = x[idx].cpu().numpy().astype(np.float64)
+    ax = oaxis(t.adjustment)
+    assert rel_err(y[idx].cpu().numpy(), O.adjusted_2d(ax, ax, xs)) < F32_TOL
