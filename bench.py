@@ -201,7 +201,7 @@ def run_reference(args, rank: int, world: int):
     per = []
     res = None
     for i in range(args.warmup + args.steps):
-        r = cpu_throughput(args.config, seconds=4.0)
+        r = cpu_throughput(args.config, seconds=2.0)
         if i >= args.warmup:
             per.append(r["value"])
             res = r
