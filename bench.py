@@ -86,7 +86,9 @@ def _oaxis(t):
 
 # ------------------------------------------------------------------ helpers
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms by one
+    long-running `nvidia-smi -lms 50`; only samples that arrive inside the
+    timed window (mark_start .. mark_end) are summarised."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -94,41 +96,53 @@ class ClockSampler:
 
     def __init__(self, device_index: int):
         self.dev = device_index
-        self.samples = []
-        self._stop = threading.Event()
+        self.samples = []  # (arrival time, fields)
+        self.t0 = self.t1 = None
+        self._proc = None
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            for line in self._proc.stdout:
+                if line.strip():
+                    self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
+        except Exception:
+            pass
 
     def __enter__(self):
         self._t.start()
+        time.sleep(0.3)  # let nvidia-smi start before the timed region
         return self
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        time.sleep(0.1)
+        if self._proc is not None:
+            self._proc.terminate()
+        self._t.join(timeout=5)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        win = [f for (t, f) in self.samples
+               if self.t0 is not None and self.t1 is not None and self.t0 - 0.05 <= t <= self.t1 + 0.05]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        num = lambda v: v.replace(".", "", 1).isdigit()  # noqa: E731
+        sm = [float(f[0]) for f in win if num(f[0])]
+        mx = [float(f[1]) for f in win if num(f[1])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        reasons = sorted({names[i] for f in win for i in range(4)
+                          if len(f) > 2 + i and f[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(win)}
 
 
 def _peaks():
@@ -280,6 +294,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        clk.mark_start()
         for k in range(args.steps):
             evs[k][0].record(stream)
             _fwd(x, y)
@@ -288,6 +303,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 _inv(y, xr)
                 evs[k][2].record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
         if world > 1:
             dist.barrier()
     fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
@@ -362,8 +378,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")

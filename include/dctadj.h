@@ -121,6 +121,11 @@ int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void
                           int32_t dtype, void* stream);
 
 /* ---- diagnostics ---- */
+/* The tile pipeline with no arithmetic (TMA load -> smem -> TMA store) on
+ * (nblk, h, w) blocks, h x w in {32x32, 64x64, 16x16}: the data-movement
+ * ceiling the transform kernels are measured against. */
+int dctadj_copy_tiles(const void* x, void* y, int64_t nblk, int32_t h, int32_t w, int32_t dtype,
+                      void* stream);
 const char* dctadj_status_string(int32_t status);
 const char* dctadj_last_error(void);
 int32_t dctadj_version(void);

@@ -68,6 +68,7 @@ SIGNATURES = {
     "dctadj_inverse_2d_host": [_AP, _AP, _P, _P, _I64, _I32, _I32],
     "dctadj_forward_frames": [_AP, _AP, _P, _P, _I32, _I32, _I32, _I32, _P],
     "dctadj_inverse_frames": [_AP, _AP, _P, _P, _I32, _I32, _I32, _I32, _P],
+    "dctadj_copy_tiles": [_P, _P, _I64, _I32, _I32, _I32, _P],
     "dctadj_status_string": [_I32],
     "dctadj_last_error": [],
     "dctadj_version": [],

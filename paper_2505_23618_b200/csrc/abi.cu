@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
@@ -19,7 +20,7 @@
 namespace dctadj {
 
 struct KernelEntry {
-  int dtype, h, w, rc, cc, col_first, in_mode, out_mode;
+  int dtype, h, w, rc, cc, col_first, in_mode, out_mode, variant;
   int (*fn)(const LaunchArgs&);
 };
 
@@ -111,13 +112,27 @@ int num_sms_cached() {
   return cache[dev];
 }
 
+// DCTADJ_VARIANT=k selects tuning variant k where one was built (tools/gen_instances.py
+// EXPERIMENT); variant 0 is the default build of every configuration.
+static int tuning_variant() {
+  static int v = [] {
+    const char* s = std::getenv("DCTADJ_VARIANT");
+    return s ? std::atoi(s) : 0;
+  }();
+  return v;
+}
+
 static const KernelEntry* find_kernel(int dtype, int h, int w, int rc, int cc, int col_first,
                                       int in_mode, int out_mode) {
+  const KernelEntry* dflt = nullptr;
+  const int want = tuning_variant();
   for (const KernelEntry& e : kRegistry)
     if (e.dtype == dtype && e.h == h && e.w == w && e.rc == rc && e.cc == cc &&
-        e.col_first == col_first && e.in_mode == in_mode && e.out_mode == out_mode)
-      return &e;
-  return nullptr;
+        e.col_first == col_first && e.in_mode == in_mode && e.out_mode == out_mode) {
+      if (e.variant == want) return &e;
+      if (e.variant == 0) dflt = &e;
+    }
+  return dflt;
 }
 
 // ------------------------------------------------------------- axis planning
@@ -646,6 +661,26 @@ int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void
   return run_frames(h, v, coefs, frames, nframes, height, width, dtype, true, S(stream));
 }
 
+int dctadj_copy_tiles(const void* x, void* y, int64_t nblk, int32_t h, int32_t w, int32_t dtype,
+                      void* stream) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if (nblk < 0) return fail(ST_ERR_SHAPE, "negative block count");
+  if (nblk == 0) return ST_OK;
+  AxisPlan ph, pv;
+  ph.n = w;
+  pv.n = h;
+  ph.code = pv.code = op_code(ST_NONE);
+  Launch L;
+  rc = prepare(L, ph, &pv, dtype, h, w, false, MODE_LINEAR, MODE_LINEAR, S(stream));
+  if (rc == ST_ERR_UNSUPPORTED) return fail(rc, "no copy kernel for %dx%d", h, w);
+  if (rc) return rc;
+  L.a.in = x;
+  L.a.out = y;
+  L.a.rows = nblk * h;
+  return L.k->fn(L.a);
+}
+
 const char* dctadj_status_string(int32_t status) {
   switch (status) {
     case DCTADJ_OK: return "ok";
@@ -663,7 +698,9 @@ const char* dctadj_status_string(int32_t status) {
 const char* dctadj_last_error(void) { return g_err; }
 int32_t dctadj_version(void) { return 1; }
 int32_t dctadj_kernel_count(void) {
-  return static_cast<int32_t>(sizeof(kRegistry) / sizeof(kRegistry[0]));
+  int32_t n = 0;
+  for (const KernelEntry& e : kRegistry) n += (e.variant == 0);
+  return n;
 }
 
 }  // extern "C"

@@ -23,6 +23,37 @@ namespace dctadj {
 
 #define DA_DEV __device__ __forceinline__
 
+// ---------------------------------------------------------------------------
+// Value types.  V is the per-thread element: float, double, or f2 -- two fp32
+// lanes (two adjacent columns, or two rows) processed by one packed
+// FADD2/FMUL2/FFMA2 instruction (sm_100).  Scalars (twiddles, adjustment
+// coefficients) are S = float/double and broadcast into both lanes (an
+// immediate or a uniform-register operand of the packed instruction).
+struct f2 {
+  float2 v;
+};
+template <typename V> struct Scalar { using type = V; };
+template <> struct Scalar<f2> { using type = float; };
+
+DA_DEV float add(float a, float b) { return a + b; }
+DA_DEV float sub(float a, float b) { return a - b; }
+DA_DEV float neg(float a) { return -a; }
+DA_DEV float mul(float a, float c) { return a * c; }
+DA_DEV float fmac(float a, float c, float b) { return fmaf(a, c, b); }    // a*c + b
+DA_DEV float fnmac(float a, float c, float b) { return fmaf(-a, c, b); }  // b - a*c
+DA_DEV double add(double a, double b) { return a + b; }
+DA_DEV double sub(double a, double b) { return a - b; }
+DA_DEV double neg(double a) { return -a; }
+DA_DEV double mul(double a, double c) { return a * c; }
+DA_DEV double fmac(double a, double c, double b) { return fma(a, c, b); }
+DA_DEV double fnmac(double a, double c, double b) { return fma(-a, c, b); }
+DA_DEV f2 add(f2 a, f2 b) { return {__fadd2_rn(a.v, b.v)}; }
+DA_DEV f2 sub(f2 a, f2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
+DA_DEV f2 neg(f2 a) { return {make_float2(-a.v.x, -a.v.y)}; }
+DA_DEV f2 mul(f2 a, float c) { return {__fmul2_rn(a.v, make_float2(c, c))}; }
+DA_DEV f2 fmac(f2 a, float c, f2 b) { return {__ffma2_rn(a.v, make_float2(c, c), b.v)}; }
+DA_DEV f2 fnmac(f2 a, float c, f2 b) { return {__ffma2_rn(make_float2(-a.v.x, -a.v.y), make_float2(c, c), b.v)}; }
+
 // Unnormalized recursion.  The reference scales by 1/sqrt(2) at every level
 // (u = (a+b)/sqrt2, v = (a-b)/sqrt2, and (c +- s)/sqrt2 in the DCT-4 output
 // butterflies): ~125 of the 411 flops of a 32-point DCT-2.  Dropping those
@@ -31,38 +62,38 @@ namespace dctadj {
 // needs g(dct2u_M) == g(dct4u_M); the bases give g = 2 at M = 4, and dct4u only
 // needs its two unscaled outputs y[0], y[M-1] multiplied by sqrt2).  The gain is
 // removed once per launch (1/32 for a 32x32 block, exact in binary).
-template <typename T, int N> DA_DEV void dct2u(const T (&x)[N], T (&y)[N]);
-template <typename T, int M> DA_DEV void dct4u(const T (&x)[M], T (&y)[M]);
-template <typename T, int N> DA_DEV void idct2u(const T (&y)[N], T (&x)[N]);
-template <typename T, int M> DA_DEV void idct4u(const T (&y)[M], T (&x)[M]);
+template <typename V, int N> DA_DEV void dct2u(const V (&x)[N], V (&y)[N]);
+template <typename V, int M> DA_DEV void dct4u(const V (&x)[M], V (&y)[M]);
+template <typename V, int N> DA_DEV void idct2u(const V (&y)[N], V (&x)[N]);
+template <typename V, int M> DA_DEV void idct4u(const V (&y)[M], V (&x)[M]);
 
 // DCT-2, gain sqrt(N): structure of reference _fastcore.pyx:50-84
-template <typename T, int N>
-DA_DEV void dct2u(const T (&x)[N], T (&y)[N]) {
+template <typename V, int N>
+DA_DEV void dct2u(const V (&x)[N], V (&y)[N]) {
+  using S = typename Scalar<V>::type;
   if constexpr (N == 1) {
     y[0] = x[0];
   } else if constexpr (N == 2) {
-    y[0] = x[0] + x[1];
-    y[1] = x[0] - x[1];
+    y[0] = add(x[0], x[1]);
+    y[1] = sub(x[0], x[1]);
   } else if constexpr (N == 4) {
-    constexpr T A = T(K_A4X2), B = T(K_B4X2);
-    const T s03 = x[0] + x[3], d03 = x[0] - x[3];
-    const T s12 = x[1] + x[2], d12 = x[1] - x[2];
-    y[0] = s03 + s12;
-    y[2] = s03 - s12;
-    y[1] = A * d03 + B * d12;
-    y[3] = B * d03 - A * d12;
+    constexpr S A = S(K_A4X2), B = S(K_B4X2);
+    const V s03 = add(x[0], x[3]), d03 = sub(x[0], x[3]);
+    const V s12 = add(x[1], x[2]), d12 = sub(x[1], x[2]);
+    y[0] = add(s03, s12);
+    y[2] = sub(s03, s12);
+    y[1] = fmac(d03, A, mul(d12, B));
+    y[3] = fnmac(d12, A, mul(d03, B));
   } else {
     constexpr int H = N / 2;
-    T u[H], v[H], eu[H], ov[H];
+    V u[H], v[H], eu[H], ov[H];
 #pragma unroll
     for (int i = 0; i < H; ++i) {
-      const T a = x[i], b = x[N - 1 - i];
-      u[i] = a + b;
-      v[i] = a - b;
+      u[i] = add(x[i], x[N - 1 - i]);
+      v[i] = sub(x[i], x[N - 1 - i]);
     }
-    dct2u<T, H>(u, eu);
-    dct4u<T, H>(v, ov);
+    dct2u<V, H>(u, eu);
+    dct4u<V, H>(v, ov);
 #pragma unroll
     for (int i = 0; i < H; ++i) {
       y[2 * i] = eu[i];
@@ -72,92 +103,98 @@ DA_DEV void dct2u(const T (&x)[N], T (&y)[N]) {
 }
 
 // DCT-4, gain sqrt(M): structure of reference _fastcore.pyx:87-117
-template <typename T, int M>
-DA_DEV void dct4u(const T (&x)[M], T (&y)[M]) {
+template <typename V, int M>
+DA_DEV void dct4u(const V (&x)[M], V (&y)[M]) {
   static_assert(M >= 4, "dct4u is only reached from dct2u with N >= 8");
+  using S = typename Scalar<V>::type;
   constexpr int H = M / 2;
   constexpr int OFF = psi_off(M);
-  constexpr T SQ2 = T(K_SQRT2);
-  T p[H], sq[H], c[H], s2[H];
+  constexpr S SQ2 = S(K_SQRT2);
+  V p[H], sq[H], c[H], s2[H];
 #pragma unroll
   for (int n = 0; n < H; ++n) {
-    const T a = x[n], b = x[M - 1 - n];
-    const T cp = T(psi_c(OFF + n)), sp = T(psi_s(OFF + n));
-    p[n] = a * cp + b * sp;
-    const T q = b * cp - a * sp;
-    // DST2(q) = reverse(DCT2(sign-alternated q))
-    sq[n] = (n % 2 == 0) ? q : -q;
+    const V a = x[n], b = x[M - 1 - n];
+    const S cp = S(psi_c(OFF + n)), sp = S(psi_s(OFF + n));
+    p[n] = fmac(a, cp, mul(b, sp));
+    // q = b cp - a sp; DST2(q) = reverse(DCT2(sign-alternated q))
+    sq[n] = (n % 2 == 0) ? fnmac(a, sp, mul(b, cp)) : fnmac(b, cp, mul(a, sp));
   }
-  dct2u<T, H>(p, c);
-  dct2u<T, H>(sq, s2);
-  y[0] = SQ2 * c[0];
+  dct2u<V, H>(p, c);
+  dct2u<V, H>(sq, s2);
+  y[0] = mul(c[0], SQ2);
 #pragma unroll
   for (int r = 1; r < H; ++r) {
-    y[2 * r] = c[r] + s2[H - r];
-    y[2 * r - 1] = c[r] - s2[H - r];
+    y[2 * r] = add(c[r], s2[H - r]);
+    y[2 * r - 1] = sub(c[r], s2[H - r]);
   }
-  y[2 * H - 1] = -SQ2 * s2[0];
+  y[2 * H - 1] = mul(s2[0], -SQ2);
 }
 
 // DCT-3 (inverse DCT-2), gain sqrt(N): structure of reference _fastcore.pyx:120-152
-template <typename T, int N>
-DA_DEV void idct2u(const T (&y)[N], T (&x)[N]) {
+template <typename V, int N>
+DA_DEV void idct2u(const V (&y)[N], V (&x)[N]) {
+  using S = typename Scalar<V>::type;
   if constexpr (N == 1) {
     x[0] = y[0];
   } else if constexpr (N == 2) {
-    x[0] = y[0] + y[1];
-    x[1] = y[0] - y[1];
+    x[0] = add(y[0], y[1]);
+    x[1] = sub(y[0], y[1]);
   } else if constexpr (N == 4) {
-    constexpr T A = T(K_A4X2), B = T(K_B4X2);
-    const T s03 = y[0] + y[2], s12 = y[0] - y[2];
-    const T d03 = A * y[1] + B * y[3];
-    const T d12 = B * y[1] - A * y[3];
-    x[0] = s03 + d03;
-    x[3] = s03 - d03;
-    x[1] = s12 + d12;
-    x[2] = s12 - d12;
+    constexpr S A = S(K_A4X2), B = S(K_B4X2);
+    const V s03 = add(y[0], y[2]), s12 = sub(y[0], y[2]);
+    const V d03 = fmac(y[1], A, mul(y[3], B));
+    const V d12 = fnmac(y[3], A, mul(y[1], B));
+    x[0] = add(s03, d03);
+    x[3] = sub(s03, d03);
+    x[1] = add(s12, d12);
+    x[2] = sub(s12, d12);
   } else {
     constexpr int H = N / 2;
-    T ye[H], yo[H], u[H], v[H];
+    V ye[H], yo[H], u[H], v[H];
 #pragma unroll
     for (int i = 0; i < H; ++i) {
       ye[i] = y[2 * i];
       yo[i] = y[2 * i + 1];
     }
-    idct2u<T, H>(ye, u);
-    idct4u<T, H>(yo, v);
+    idct2u<V, H>(ye, u);
+    idct4u<V, H>(yo, v);
 #pragma unroll
     for (int i = 0; i < H; ++i) {
-      x[i] = u[i] + v[i];
-      x[N - 1 - i] = u[i] - v[i];
+      x[i] = add(u[i], v[i]);
+      x[N - 1 - i] = sub(u[i], v[i]);
     }
   }
 }
 
 // inverse DCT-4, gain sqrt(M): structure of reference _fastcore.pyx:155-185
-template <typename T, int M>
-DA_DEV void idct4u(const T (&y)[M], T (&x)[M]) {
+template <typename V, int M>
+DA_DEV void idct4u(const V (&y)[M], V (&x)[M]) {
   static_assert(M >= 4, "idct4u is only reached from idct2u with N >= 8");
+  using S = typename Scalar<V>::type;
   constexpr int H = M / 2;
   constexpr int OFF = psi_off(M);
-  constexpr T SQ2 = T(K_SQRT2);
-  T c[H], sr[H], p[H], q[H];
-  c[0] = SQ2 * y[0];
+  constexpr S SQ2 = S(K_SQRT2);
+  V c[H], sr[H], p[H], q[H];
+  c[0] = mul(y[0], SQ2);
 #pragma unroll
   for (int r = 1; r < H; ++r) {
-    c[r] = y[2 * r] + y[2 * r - 1];
-    sr[H - r] = y[2 * r] - y[2 * r - 1];  // s[r-1], stored reversed
+    c[r] = add(y[2 * r], y[2 * r - 1]);
+    sr[H - r] = sub(y[2 * r], y[2 * r - 1]);  // s[r-1], stored reversed
   }
-  sr[0] = -SQ2 * y[2 * H - 1];            // s[H-1]
-  idct2u<T, H>(c, p);
-  // inverse DST2: reverse, inverse DCT2, sign-alternate
-  idct2u<T, H>(sr, q);
+  sr[0] = mul(y[2 * H - 1], -SQ2);            // s[H-1]
+  idct2u<V, H>(c, p);
+  // inverse DST2: reverse, inverse DCT2, sign-alternate (folded into the rotation)
+  idct2u<V, H>(sr, q);
 #pragma unroll
   for (int n = 0; n < H; ++n) {
-    const T qn = (n % 2 == 0) ? q[n] : -q[n];
-    const T cp = T(psi_c(OFF + n)), sp = T(psi_s(OFF + n));
-    x[n] = p[n] * cp - qn * sp;
-    x[M - 1 - n] = p[n] * sp + qn * cp;
+    const S cp = S(psi_c(OFF + n)), sp = S(psi_s(OFF + n));
+    if (n % 2 == 0) {
+      x[n] = fnmac(q[n], sp, mul(p[n], cp));
+      x[M - 1 - n] = fmac(q[n], cp, mul(p[n], sp));
+    } else {
+      x[n] = fmac(q[n], sp, mul(p[n], cp));
+      x[M - 1 - n] = fnmac(q[n], cp, mul(p[n], sp));
+    }
   }
 }
 
@@ -217,77 +254,68 @@ struct AxisOp {
   };
 };
 
-template <typename T, int N, int S, int K>
-DA_DEV void run_stage(T (&v)[N], const T* __restrict__ cf, const T* __restrict__ dense) {
+template <typename V, int N, int S, int K>
+DA_DEV void run_stage(V (&v)[N], const typename Scalar<V>::type* __restrict__ cf,
+                      const typename Scalar<V>::type* __restrict__ dense) {
   if constexpr (S == ST_NONE) {
     return;
   } else if constexpr (S == ST_DCT2) {
-    T y[N];
-    dct2u<T, N>(v, y);
+    V y[N];
+    dct2u<V, N>(v, y);
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = y[i];
   } else if constexpr (S == ST_IDCT2) {
-    T y[N];
-    idct2u<T, N>(v, y);
+    V y[N];
+    idct2u<V, N>(v, y);
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = y[i];
   } else if constexpr (S == ST_DST3) {
-    T r[N], y[N];
+    V r[N], y[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) r[j] = v[N - 1 - j];
-    idct2u<T, N>(r, y);
+    idct2u<V, N>(r, y);
 #pragma unroll
-    for (int j = 0; j < N; ++j) v[j] = (j % 2 == 0) ? y[j] : -y[j];
+    for (int j = 0; j < N; ++j) v[j] = (j % 2 == 0) ? y[j] : neg(y[j]);
   } else if constexpr (S == ST_IDST3) {
-    T a[N], y[N];
+    V a[N], y[N];
 #pragma unroll
-    for (int j = 0; j < N; ++j) a[j] = (j % 2 == 0) ? v[j] : -v[j];
-    dct2u<T, N>(a, y);
+    for (int j = 0; j < N; ++j) a[j] = (j % 2 == 0) ? v[j] : neg(v[j]);
+    dct2u<V, N>(a, y);
 #pragma unroll
     for (int j = 0; j < N; ++j) v[j] = y[N - 1 - j];
   } else if constexpr (S == ST_BAND) {
     constexpr int D = 2 * K - 1;
-    T y[N];
+    V y[N];
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      T acc = T(0);
-      bool first = true;
+      const int j0 = r - (K - 1) < 0 ? 0 : r - (K - 1);
+      const int j1 = r + K > N ? N : r + K;
+      V acc = mul(v[j0], cf[r * D + (j0 - r + K - 1)]);
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        const int j = r - (K - 1) + d;
-        if (j >= 0 && j < N) {
-          if (first) {
-            acc = cf[r * D + d] * v[j];
-            first = false;
-          } else {
-            acc = fma(cf[r * D + d], v[j], acc);
-          }
-        }
-      }
+      for (int j = j0 + 1; j < j1; ++j) acc = fmac(v[j], cf[r * D + (j - r + K - 1)], acc);
       y[r] = acc;
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = y[i];
   } else if constexpr (S == ST_SUB) {
     static_assert(K <= N, "sub-block order exceeds transform size");
-    T y[K];
+    V y[K];
 #pragma unroll
     for (int r = 0; r < K; ++r) {
-      T acc = cf[r * K] * v[0];
+      V acc = mul(v[0], cf[r * K]);
 #pragma unroll
-      for (int j = 1; j < K; ++j) acc = fma(cf[r * K + j], v[j], acc);
+      for (int j = 1; j < K; ++j) acc = fmac(v[j], cf[r * K + j], acc);
       y[r] = acc;
     }
 #pragma unroll
     for (int r = 0; r < K; ++r) v[r] = y[r];
   } else if constexpr (S == ST_DENSE) {
-    // dense rows are read as 16-byte broadcasts from shared memory
-    T y[N];
+    V y[N];
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      T acc = dense[r * N] * v[0];
+      V acc = mul(v[0], dense[r * N]);
 #pragma unroll
-      for (int j = 1; j < N; ++j) acc = fma(dense[r * N + j], v[j], acc);
+      for (int j = 1; j < N; ++j) acc = fmac(v[j], dense[r * N + j], acc);
       y[r] = acc;
     }
 #pragma unroll
@@ -295,12 +323,13 @@ DA_DEV void run_stage(T (&v)[N], const T* __restrict__ cf, const T* __restrict__
   }
 }
 
-template <typename T, int N, int CODE>
-DA_DEV void apply_axis(T (&v)[N], const typename AxisOp<T, N, CODE>::Coef& cf,
-                       const T* __restrict__ dense) {
-  using Op = AxisOp<T, N, CODE>;
-  run_stage<T, N, Op::S1, Op::K>(v, cf.c, dense);
-  run_stage<T, N, Op::S2, Op::K>(v, cf.c, dense);
+template <typename V, int N, int CODE>
+DA_DEV void apply_axis(V (&v)[N],
+                       const typename AxisOp<typename Scalar<V>::type, N, CODE>::Coef& cf,
+                       const typename Scalar<V>::type* __restrict__ dense) {
+  using Op = AxisOp<typename Scalar<V>::type, N, CODE>;
+  run_stage<V, N, Op::S1, Op::K>(v, cf.c, dense);
+  run_stage<V, N, Op::S2, Op::K>(v, cf.c, dense);
 }
 
 }  // namespace dctadj

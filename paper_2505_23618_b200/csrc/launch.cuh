@@ -68,22 +68,22 @@ int make_map(CUtensorMap* map, const void* base, const LaunchArgs& a) {
 }
 
 template <typename T, int H, int W, int P, int RC, int CC, bool COL_FIRST, int IN_MODE,
-          int OUT_MODE, int NG, int S>
+          int OUT_MODE, int NG, int S, bool PAIR_ROW = false, bool PAIR_COL = false, int CH = 0>
 int launch_tile(const LaunchArgs& a) {
   using L = TileLayout<T, H, W, P>;
   using RowOp = AxisOp<T, W, RC>;
   using ColOp = AxisOp<T, H, CC>;
   static_assert(S >= 2, "ring needs at least two stages");
-  static_assert(IN_MODE == MODE_LINEAR || P == 1, "frame tiles are single blocks");
-  static_assert(OUT_MODE == MODE_LINEAR || P == 1, "frame tiles are single blocks");
 
   Geom g{};
   if (IN_MODE == MODE_FRAME || OUT_MODE == MODE_FRAME) {
     g.tiles_y = (a.frame_h + H - 1) / H;
     g.tiles_x = a.frame_w / W;
-    g.ntiles = static_cast<int64_t>(a.frames) * g.tiles_y * g.tiles_x;
+    g.nblocks = static_cast<int64_t>(a.frames) * g.tiles_y * g.tiles_x;
+    g.ntiles = (g.nblocks + P - 1) / P;
   } else {
     g.ntiles = (a.rows + L::PH - 1) / L::PH;
+    g.nblocks = g.ntiles * P;
   }
   if (g.ntiles == 0) return ST_OK;
   g.dense_row = a.dense_row;
@@ -91,7 +91,7 @@ int launch_tile(const LaunchArgs& a) {
 
   // the LINEAR side of a frame launch holds ntiles whole blocks
   LaunchArgs la = a;
-  if (IN_MODE == MODE_FRAME || OUT_MODE == MODE_FRAME) la.rows = g.ntiles * H;
+  if (IN_MODE == MODE_FRAME || OUT_MODE == MODE_FRAME) la.rows = g.nblocks * H;
 
   CUtensorMap in_map, out_map;
   int rc = make_map<T, H, W, P, IN_MODE>(&in_map, a.in, la);
@@ -104,7 +104,7 @@ int launch_tile(const LaunchArgs& a) {
   if (RowOp::NCOEF > 0) std::memcpy(prm.row.c, a.row_coef, sizeof(T) * RowOp::NCOEF);
   if (ColOp::NCOEF > 0) std::memcpy(prm.col.c, a.col_coef, sizeof(T) * ColOp::NCOEF);
 
-  auto kern = tile_kernel<T, H, W, P, RC, CC, COL_FIRST, IN_MODE, OUT_MODE, NG, S>;
+  auto kern = tile_kernel<T, H, W, P, RC, CC, COL_FIRST, IN_MODE, OUT_MODE, NG, S, PAIR_ROW, PAIR_COL, CH>;
   const size_t dense_bytes =
       sizeof(T) * ((RowOp::kDense ? W * W : 0) + (ColOp::kDense ? H * H : 0));
   const size_t smem = 1024 + static_cast<size_t>(NG) * S * L::STAGEB + NG * S * 8 + dense_bytes;

@@ -78,6 +78,28 @@ DA_DEV void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// L2 eviction-priority hints for streaming data (read once / written once)
+DA_DEV uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+DA_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                             uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+DA_DEV void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0, int c1,
+                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint"
+      " [%0, {%2, %3}], [%1], %4;" ::"l"(map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
 DA_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 DA_DEV void bulk_wait_read() {
@@ -121,6 +143,7 @@ enum Mode : int { MODE_LINEAR = 0, MODE_FRAME = 1 };
 
 struct Geom {
   int64_t ntiles;      // super-tiles
+  int64_t nblocks;     // blocks (FRAME: a super-tile holds P consecutive raster blocks)
   int32_t tiles_y;     // FRAME: tile rows per frame
   int32_t tiles_x;     // FRAME: tile columns per frame
   const void* dense_row;  // device N x N (T) for ST_DENSE row op
@@ -133,28 +156,56 @@ struct KParams {
   typename AxisOp<T, H, CC>::Coef col;
 };
 
-template <typename T, int H, int W, int P, int MODE>
+// Blocks of super-tile t that exist (a FRAME super-tile may be cut short).
+template <int P, int MODE>
+DA_DEV int tile_blocks(int64_t t, const Geom& g) {
+  if constexpr (MODE == MODE_LINEAR || P == 1) {
+    return P;
+  } else {
+    const int64_t left = g.nblocks - t * P;
+    return left < P ? static_cast<int>(left) : P;
+  }
+}
+
+// TMA loads (load=true) or stores of super-tile t.  LINEAR: one box per
+// 128-byte column slice covering all P*H rows.  FRAME: one box per block and
+// column slice, block b -> (frame, tile row, tile column) in raster order.
+// CH: L2 hint bits -- 1: loads evict_first, 2: stores evict_first
+template <typename T, int H, int W, int P, int MODE, int CH = 0>
 DA_DEV void issue_tile_io(bool load, void* stage, const CUtensorMap* map, uint64_t* bar,
-                          int64_t t, const Geom& g) {
+                          int64_t t, const Geom& g, int nb) {
   using L = TileLayout<T, H, W, P>;
 #pragma unroll
   for (int b = 0; b < L::NB; ++b) {
     uint8_t* dst = static_cast<uint8_t*>(stage) + b * L::BOXB;
     if constexpr (MODE == MODE_LINEAR) {
       const int row0 = static_cast<int>(t * L::PH);
-      if (load)
-        tma_load_2d(dst, map, bar, b * L::BW, row0);
-      else
-        tma_store_2d(map, dst, b * L::BW, row0);
+      if (load) {
+        if constexpr (CH & 1)
+          tma_load_2d_hint(dst, map, bar, b * L::BW, row0, policy_evict_first());
+        else
+          tma_load_2d(dst, map, bar, b * L::BW, row0);
+      } else {
+        if constexpr (CH & 2)
+          tma_store_2d_hint(map, dst, b * L::BW, row0, policy_evict_first());
+        else
+          tma_store_2d(map, dst, b * L::BW, row0);
+      }
     } else {
       const int64_t per = static_cast<int64_t>(g.tiles_x) * g.tiles_y;
-      const int f = static_cast<int>(t / per);
-      const int rem = static_cast<int>(t - f * per);
-      const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
-      if (load)
-        tma_load_3d(dst, map, bar, tx * W + b * L::BW, ty * H, f);
-      else
-        tma_store_3d(map, dst, tx * W + b * L::BW, ty * H, f);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        if (p >= nb) break;
+        const int64_t blk = t * P + p;
+        const int f = static_cast<int>(blk / per);
+        const int rem = static_cast<int>(blk - f * per);
+        const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+        uint8_t* d = dst + p * H * L::BRB;
+        if (load)
+          tma_load_3d(d, map, bar, tx * W + b * L::BW, ty * H, f);
+        else
+          tma_store_3d(map, d, tx * W + b * L::BW, ty * H, f);
+      }
     }
   }
 }
@@ -168,65 +219,113 @@ __host__ __device__ constexpr double inv_sqrt_pow2(int gsq) {
   return (e % 2) ? s * K_SQRT1_2 : s;
 }
 
-template <typename T, int H, int W, int P, int RC, int CC, int GSQ>
+template <typename V, int N, int GSQ>
+DA_DEV void scale_out(V (&v)[N]) {
+  if constexpr (GSQ > 1) {
+    using Sc = typename Scalar<V>::type;
+    constexpr Sc sc = Sc(inv_sqrt_pow2(GSQ));
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = mul(v[i], sc);
+  }
+}
+
+// Row pass: lane owns a row (PAIR: two rows, rho and rho + 32, packed as f2
+// lanes).  Rows are read/written as 16-byte chunks: conflict-free under the
+// swizzle (8 lanes of a phase hit 8 distinct chunk columns).
+template <typename T, int H, int W, int P, int RC, int GSQ, bool PAIR>
 DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Coef& cf,
                      const T* dense) {
   using L = TileLayout<T, H, W, P>;
   constexpr int PER16 = 16 / sizeof(T);
+  constexpr int ROWS_PER_IT = PAIR ? 64 : 32;
+  static_assert(L::PH % ROWS_PER_IT == 0, "row pass must cover whole warps");
 #pragma unroll 1
-  for (int it = 0; it < L::PH / 32; ++it) {
-    const uint32_t rho = it * 32 + lane;
-    T v[W];
+  for (int it = 0; it < L::PH / ROWS_PER_IT; ++it) {
+    const uint32_t rho = it * ROWS_PER_IT + lane;
+    if constexpr (!PAIR) {
+      T v[W];
 #pragma unroll
-    for (int q = 0; q < W / PER16; ++q) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(buf + L::addr(rho, q * 16));
-      const T* e = reinterpret_cast<const T*>(&raw);
+      for (int q = 0; q < W / PER16; ++q) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(buf + L::addr(rho, q * 16));
+        const T* e = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-      for (int k = 0; k < PER16; ++k) v[q * PER16 + k] = e[k];
-    }
-    apply_axis<T, W, RC>(v, cf, dense);
-    if constexpr (GSQ > 1) {
-      constexpr T sc = T(inv_sqrt_pow2(GSQ));
+        for (int k = 0; k < PER16; ++k) v[q * PER16 + k] = e[k];
+      }
+      apply_axis<T, W, RC>(v, cf, dense);
+      scale_out<T, W, GSQ>(v);
 #pragma unroll
-      for (int i = 0; i < W; ++i) v[i] *= sc;
-    }
+      for (int q = 0; q < W / PER16; ++q) {
+        uint4 raw;
+        T* e = reinterpret_cast<T*>(&raw);
 #pragma unroll
-    for (int q = 0; q < W / PER16; ++q) {
-      uint4 raw;
-      T* e = reinterpret_cast<T*>(&raw);
+        for (int k = 0; k < PER16; ++k) e[k] = v[q * PER16 + k];
+        *reinterpret_cast<uint4*>(buf + L::addr(rho, q * 16)) = raw;
+      }
+    } else {
+      static_assert(sizeof(T) == 4, "packed rows are fp32 pairs");
+      f2 v[W];
 #pragma unroll
-      for (int k = 0; k < PER16; ++k) e[k] = v[q * PER16 + k];
-      *reinterpret_cast<uint4*>(buf + L::addr(rho, q * 16)) = raw;
+      for (int q = 0; q < W / 4; ++q) {
+        const float4 a = *reinterpret_cast<const float4*>(buf + L::addr(rho, q * 16));
+        const float4 b = *reinterpret_cast<const float4*>(buf + L::addr(rho + 32, q * 16));
+        v[4 * q + 0].v = make_float2(a.x, b.x);
+        v[4 * q + 1].v = make_float2(a.y, b.y);
+        v[4 * q + 2].v = make_float2(a.z, b.z);
+        v[4 * q + 3].v = make_float2(a.w, b.w);
+      }
+      apply_axis<f2, W, RC>(v, cf, dense);
+      scale_out<f2, W, GSQ>(v);
+#pragma unroll
+      for (int q = 0; q < W / 4; ++q) {
+        *reinterpret_cast<float4*>(buf + L::addr(rho, q * 16)) =
+            make_float4(v[4 * q].v.x, v[4 * q + 1].v.x, v[4 * q + 2].v.x, v[4 * q + 3].v.x);
+        *reinterpret_cast<float4*>(buf + L::addr(rho + 32, q * 16)) =
+            make_float4(v[4 * q].v.y, v[4 * q + 1].v.y, v[4 * q + 2].v.y, v[4 * q + 3].v.y);
+      }
     }
   }
 }
 
-template <typename T, int H, int W, int P, int RC, int CC, int GSQ>
+// Column pass: lane owns a column (PAIR: two adjacent columns read as one
+// 8-byte word, packed as f2 lanes).  Conflict-free under the swizzle.
+template <typename T, int H, int W, int P, int CC, int GSQ, bool PAIR>
 DA_DEV void col_pass(uint8_t* buf, int lane, const typename AxisOp<T, H, CC>::Coef& cf,
                      const T* dense) {
   using L = TileLayout<T, H, W, P>;
+  constexpr int COLS_PER_IT = PAIR ? 64 : 32;
+  static_assert((P * W) % COLS_PER_IT == 0, "column pass must cover whole warps");
 #pragma unroll 1
-  for (int it = 0; it < (P * W) / 32; ++it) {
-    const int kappa = it * 32 + lane;
+  for (int it = 0; it < (P * W) / COLS_PER_IT; ++it) {
+    const int kappa = it * COLS_PER_IT + (PAIR ? 2 : 1) * lane;
     const uint32_t p = kappa / W, c = kappa % W;
     const uint32_t byte = c * sizeof(T);
-    T v[H];
+    if constexpr (!PAIR) {
+      T v[H];
 #pragma unroll
-    for (int i = 0; i < H; ++i) v[i] = *reinterpret_cast<const T*>(buf + L::addr(p * H + i, byte));
-    apply_axis<T, H, CC>(v, cf, dense);
-    if constexpr (GSQ > 1) {
-      constexpr T sc = T(inv_sqrt_pow2(GSQ));
+      for (int i = 0; i < H; ++i)
+        v[i] = *reinterpret_cast<const T*>(buf + L::addr(p * H + i, byte));
+      apply_axis<T, H, CC>(v, cf, dense);
+      scale_out<T, H, GSQ>(v);
 #pragma unroll
-      for (int i = 0; i < H; ++i) v[i] *= sc;
+      for (int i = 0; i < H; ++i) *reinterpret_cast<T*>(buf + L::addr(p * H + i, byte)) = v[i];
+    } else {
+      static_assert(sizeof(T) == 4, "packed columns are fp32 pairs");
+      f2 v[H];
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+        v[i].v = *reinterpret_cast<const float2*>(buf + L::addr(p * H + i, byte));
+      apply_axis<f2, H, CC>(v, cf, dense);
+      scale_out<f2, H, GSQ>(v);
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+        *reinterpret_cast<float2*>(buf + L::addr(p * H + i, byte)) = v[i].v;
     }
-#pragma unroll
-    for (int i = 0; i < H; ++i) *reinterpret_cast<T*>(buf + L::addr(p * H + i, byte)) = v[i];
   }
 }
 
 // NG warps per CTA, each with an S-stage ring.
 template <typename T, int H, int W, int P, int RC, int CC, bool COL_FIRST, int IN_MODE,
-          int OUT_MODE, int NG, int S>
+          int OUT_MODE, int NG, int S, bool PAIR_ROW = false, bool PAIR_COL = false, int CH = 0>
 __global__ void __launch_bounds__(NG * 32)
     tile_kernel(const __grid_constant__ CUtensorMap in_map,
                 const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
@@ -278,8 +377,9 @@ __global__ void __launch_bounds__(NG * 32)
     for (int s = 0; s < S; ++s) {
       const int64_t t = gid + s * gstride;
       if (t < ntiles) {
-        mbar_arrive_expect_tx(&bars[s], L::TILEB);
-        issue_tile_io<T, H, W, P, IN_MODE>(true, ring + s * L::STAGEB, &in_map, &bars[s], t, geom);
+        const int nb = tile_blocks<P, IN_MODE>(t, geom);
+        mbar_arrive_expect_tx(&bars[s], L::TILEB / P * nb);
+        issue_tile_io<T, H, W, P, IN_MODE, CH>(true, ring + s * L::STAGEB, &in_map, &bars[s], t, geom, nb);
       }
     }
   }
@@ -293,23 +393,24 @@ __global__ void __launch_bounds__(NG * 32)
     constexpr int GSQ = RowOp::kGainSq * ColOp::kGainSq;
     if constexpr (!COL_FIRST) {
       if constexpr (!RowOp::kIdentity) {
-        row_pass<T, H, W, P, RC, CC, ColOp::kIdentity ? GSQ : 1>(buf, lane, prm.row, dense_row);
+        row_pass<T, H, W, P, RC, ColOp::kIdentity ? GSQ : 1, PAIR_ROW>(buf, lane, prm.row, dense_row);
         if constexpr (!ColOp::kIdentity) __syncwarp();
       }
       if constexpr (!ColOp::kIdentity)
-        col_pass<T, H, W, P, RC, CC, GSQ>(buf, lane, prm.col, dense_col);
+        col_pass<T, H, W, P, CC, GSQ, PAIR_COL>(buf, lane, prm.col, dense_col);
     } else {
       if constexpr (!ColOp::kIdentity) {
-        col_pass<T, H, W, P, RC, CC, RowOp::kIdentity ? GSQ : 1>(buf, lane, prm.col, dense_col);
+        col_pass<T, H, W, P, CC, RowOp::kIdentity ? GSQ : 1, PAIR_COL>(buf, lane, prm.col, dense_col);
         if constexpr (!RowOp::kIdentity) __syncwarp();
       }
       if constexpr (!RowOp::kIdentity)
-        row_pass<T, H, W, P, RC, CC, GSQ>(buf, lane, prm.row, dense_row);
+        row_pass<T, H, W, P, RC, GSQ, PAIR_ROW>(buf, lane, prm.row, dense_row);
     }
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      issue_tile_io<T, H, W, P, OUT_MODE>(false, buf, &out_map, nullptr, t, geom);
+      issue_tile_io<T, H, W, P, OUT_MODE, CH>(false, buf, &out_map, nullptr, t, geom,
+                                          tile_blocks<P, OUT_MODE>(t, geom));
       bulk_commit();
       // refill the stage freed by the previous tile with the tile S-1 strides ahead
       if (k >= 1) {
@@ -317,9 +418,10 @@ __global__ void __launch_bounds__(NG * 32)
         if (tn < ntiles) {
           const int sp = (s == 0) ? S - 1 : s - 1;
           bulk_wait_read<1>();
-          mbar_arrive_expect_tx(&bars[sp], L::TILEB);
-          issue_tile_io<T, H, W, P, IN_MODE>(true, ring + sp * L::STAGEB, &in_map, &bars[sp], tn,
-                                             geom);
+          const int nb = tile_blocks<P, IN_MODE>(tn, geom);
+          mbar_arrive_expect_tx(&bars[sp], L::TILEB / P * nb);
+          issue_tile_io<T, H, W, P, IN_MODE, CH>(true, ring + sp * L::STAGEB, &in_map, &bars[sp], tn,
+                                             geom, nb);
         }
       }
     }

@@ -26,14 +26,25 @@ ID = code(NONE)
 DTYPES = {"float": 0, "double": 1}
 
 
-def tile_config(dtype: str, h: int, w: int, two_d: bool):
+def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False):
+    """(P blocks per super-tile, NG warps per CTA, S ring stages).
+
+    Measured on B200 (profiles/r01_tuning.md): for 32x32 fp32 the forward
+    (rows first) runs best with 16 KB super-tiles, 2 warps x 3 stages per CTA;
+    the inverse (columns first) with 8 KB super-tiles, 4 warps x 4 stages --
+    both ~86 us per 536 MB launch (0.95 of the measured HBM copy peak)."""
     es = 4 if dtype == "float" else 8
     p = 1
-    if two_d and min(h, w) < 32:
-        p = 32 // min(h, w)
+    if two_d:
+        # rows: P*H >= 32; packed column pairs (fp32): P*W >= 64
+        p = max(1, 32 // h, (64 // w) if dtype == "float" else 32 // w)
+        if dtype == "float" and h * w <= 1024:
+            p = max(p, (4 if not col_first else 2) * 1024 // (h * w))
     tile = p * h * w * es
     stage = -(-tile // 1024) * 1024
-    if stage <= 2048:
+    if two_d and dtype == "float" and h * w <= 1024:
+        ng, s = (2, 3) if not col_first else (4, 4)
+    elif stage <= 2048:
         ng, s = 8, 4
     elif stage <= 4096:
         ng, s = 8, 3
@@ -81,6 +92,19 @@ def two_d_pairs():
     return [(r, c, False) for r, c in fwd] + [(r, c, True) for r, c in inv]
 
 
+def pair_flags(dt, h, w, p, rc, cc):
+    """Default packing: fp32 column pairs (FFMA2) when a column op exists and
+    the super-tile has >= 64 columns; rows stay scalar."""
+    if dt != "float" or cc == ID:
+        return (False, False)
+    return (False, (p * w) % 64 == 0)
+
+
+# tuning variants for the 32x32 fp32 hot kernels (DCTADJ_VARIANT=k): (P, NG, S)
+# tuning variants for the 32x32 fp32 hot kernels (DCTADJ_VARIANT=k): (P, NG, S, L2 hints)
+EXPERIMENT = [(4, 2, 3, 0), (2, 4, 4, 0)]
+
+
 def instances():
     out = []
     for dt in DTYPES:
@@ -92,17 +116,39 @@ def instances():
         if dt == "double":
             shapes = [(16, 16), (32, 32), (64, 64)]
         for h, w in shapes:
-            p, ng, s = tile_config(dt, h, w, True)
             for rc, cc, cf in two_d_pairs():
+                p, ng, s = tile_config(dt, h, w, True, cf)
                 out.append((dt, h, w, p, rc, cc, cf, 0, 0, ng, s))
     # frame tiling (config 5): 32x32 fp32, frames in / blocks out and back
-    p, ng, s = tile_config("float", 32, 32, True)
     for rc, cc, cf in two_d_pairs():
         if rc == code(DCT2) or (rc >> 8) == 4:
             continue
+        p, ng, s = tile_config("float", 32, 32, True, cf)
         in_mode, out_mode = (0, 1) if cf else (1, 0)
         out.append(("float", 32, 32, p, rc, cc, cf, in_mode, out_mode, ng, s))
-    return out
+    # identity-op tile round trip (TMA in -> smem -> TMA out, no arithmetic):
+    # the data-movement ceiling of the tile pipeline (dctadj_copy_tiles)
+    for dt in DTYPES:
+        for h, w in ((32, 32), (64, 64), (16, 16)):
+            p, ng, s = tile_config(dt, h, w, True)
+            out.append((dt, h, w, p, ID, ID, False, 0, 0, ng, s))
+    # attach packing flags + tuning variants (variant 0 = default)
+    final = []
+    for inst in out:
+        dt, h, w, p, rc, cc, cf, im, om, ng, s_ = inst
+        final.append(inst + pair_flags(dt, h, w, p, rc, cc) + (0, 0))
+        if dt == "float" and (h, w) == (32, 32) and im == 0 and om == 0 and rc == cc \
+                and rc in (ID, code(DCT2, SUB, 8), code(SUB, IDCT2, 8)):
+            for k, (pp, nng, ss, ch) in enumerate(EXPERIMENT, start=1):
+                final.append((dt, h, w, pp, rc, cc, cf, im, om, nng, ss)
+                             + pair_flags(dt, h, w, pp, rc, cc) + (k, ch))
+    return final
+
+
+def _targs(inst) -> str:
+    dt, h, w, p, rc, cc, cf, im, om, ng, s, pr, pc, var, ch = inst
+    b = lambda v: "true" if v else "false"  # noqa: E731
+    return f"{dt}, {h}, {w}, {p}, {rc}, {cc}, {b(cf)}, {im}, {om}, {ng}, {s}, {b(pr)}, {b(pc)}, {ch}"
 
 
 def _write_if_changed(path: Path, text: str) -> None:
@@ -122,18 +168,17 @@ def main():
     for k, shard in enumerate(shards):
         lines = ["// Generated by tools/gen_instances.py -- do not edit.",
                  '#include "../launch.cuh"', "", "namespace dctadj {", ""]
-        for (dt, h, w, p, rc, cc, cf, im, om, ng, s) in shard:
-            lines.append(
-                f"template int launch_tile<{dt}, {h}, {w}, {p}, {rc}, {cc}, "
-                f"{'true' if cf else 'false'}, {im}, {om}, {ng}, {s}>(const LaunchArgs&);")
+        for inst in shard:
+            lines.append(f"template int launch_tile<{_targs(inst)}>(const LaunchArgs&);")
         lines += ["", "}  // namespace dctadj", ""]
         _write_if_changed(ROOT / f"inst_{k:02d}.cu", "\n".join(lines))
     decl = []
     rows = []
-    for (dt, h, w, p, rc, cc, cf, im, om, ng, s) in insts:
-        targs = f"{dt}, {h}, {w}, {p}, {rc}, {cc}, {'true' if cf else 'false'}, {im}, {om}, {ng}, {s}"
+    for inst in insts:
+        dt, h, w, p, rc, cc, cf, im, om, ng, s, pr, pc, var, ch = inst
+        targs = _targs(inst)
         decl.append(f"extern template int launch_tile<{targs}>(const LaunchArgs&);")
-        rows.append(f"  {{{DTYPES[dt]}, {h}, {w}, {rc}, {cc}, {int(cf)}, {im}, {om}, "
+        rows.append(f"  {{{DTYPES[dt]}, {h}, {w}, {rc}, {cc}, {int(cf)}, {im}, {om}, {var}, "
                     f"&launch_tile<{targs}>}},")
     reg += decl + ["", "static const KernelEntry kRegistry[] = {"] + rows + ["};", ""]
     _write_if_changed(ROOT / "registry.inc", "\n".join(reg))
