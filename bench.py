@@ -12,6 +12,9 @@ One step = forward_adjusted_2d then inverse_adjusted_2d over the batch, each one
 fused kernel (rows + columns + adjustment).  Inputs are 268 MB per GPU (> the
 126 MB L2), so no flush is needed between steps.
 
+The other configs (--config c1 | c3_pre | c3_post | c4_{dst7,dct8}_{pre,post} |
+c5) are parity cases of BASELINE.json measured the same way (no bench line).
+
 Multi-GPU (torchrun): every rank runs the same per-GPU workload on its own
 block range (weak scaling, no data-path collective); timing is CUDA events on
 the launching stream, max over ranks (NCCL all_reduce of scalars only).
@@ -19,8 +22,8 @@ the launching stream, max over ranks (NCCL all_reduce of scalars only).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
-import math
 import os
 import subprocess
 import sys
@@ -37,42 +40,24 @@ METRIC = "transform coeffs/sec (fwd+inv) at 1/2/4/8 B200; % of HBM roofline vs C
 UNIT = "coef/s"
 
 
-# ------------------------------------------------------------------ configs
-def _c2_transforms():
-    from paper_2505_23618_b200 import matio, pipeline
+# ------------------------------------------------------------------ adjustments
+def _t(adj):
+    from paper_2505_23618_b200 import pipeline
+    return pipeline.make_adjusted_transform(adj)
+
+
+def _post(n, kind):
+    from paper_2505_23618_b200 import matio
     from paper_2505_23618_b200.design import dct8_adjustment_from_dst7
-    t = pipeline.make_adjusted_transform(
-        dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32")))
-    return t, t
+    a = matio.load_designed(f"sub8_post_dct2_dst7_n{n}")
+    return _t(a if kind == "dst7" else dct8_adjustment_from_dst7(a))
 
 
-def _c1_transforms():
-    from paper_2505_23618_b200 import matio, pipeline
-    t = pipeline.make_adjusted_transform(matio.load_designed("band6_pre_dst3_dst7_n32"))
-    return t, t
-
-
-def _c4_transforms(variant):
-    from paper_2505_23618_b200 import matio, pipeline
-    from paper_2505_23618_b200.design import dct8_adjustment_from_dst7, flip_pre_adjustment
-    b6 = matio.load_designed("band6_pre_dst3_dst7_n64")
-    s7 = matio.load_designed("sub8_post_dct2_dst7_n64")
-    adj = {"dst7_pre": b6, "dct8_pre": flip_pre_adjustment(b6), "dst7_post": s7,
-           "dct8_post": dct8_adjustment_from_dst7(s7)}[variant]
-    t = pipeline.make_adjusted_transform(adj)
-    return t, t
-
-
-CONFIGS = {
-    "c2": dict(workload="c2_dct8_post_sub8_n32_fwd+inv_65536x32x32", blocks=65536, h=32, w=32,
-               dtype="f32", transforms=_c2_transforms, inputs="c2_inputs", inverse=True),
-    "c1": dict(workload="c1_dst7_pre_band6_n32_fwd_4096x32x32", blocks=4096, h=32, w=32,
-               dtype="f64", transforms=_c1_transforms, inputs="c1_inputs", inverse=False),
-}
-for _v in ("dst7_pre", "dct8_pre", "dst7_post", "dct8_post"):
-    CONFIGS[f"c4_{_v}"] = dict(workload=f"c4_{_v}_n64_fwd+inv_262144x64x64", blocks=262144, h=64,
-                               w=64, dtype="f32", transforms=(lambda v=_v: _c4_transforms(v)),
-                               inputs="c4_inputs", inverse=True)
+def _pre(n, kind):
+    from paper_2505_23618_b200 import matio
+    from paper_2505_23618_b200.design import flip_pre_adjustment
+    a = matio.load_designed(f"band6_pre_dst3_dst7_n{n}")
+    return _t(a if kind == "dst7" else flip_pre_adjustment(a))
 
 
 def _oaxis(t):
@@ -82,6 +67,21 @@ def _oaxis(t):
     kind = {"band": O.ADJ_BAND, "subblock": O.ADJ_SUBBLOCK, "dense": O.ADJ_DENSE}[adj.pattern.kind.value]
     return O.OAxis(adj.pattern.size, base, kind, O.SIDE_PRE if adj.side.value == "pre" else O.SIDE_POST,
                    adj.pattern.taps or 0, adj.pattern.order or 0, np.array(adj.realized))
+
+
+# uniform-block configs: (workload, blocks, H=W, dtype, transform factory, inputs, inverse?)
+UNIFORM = {
+    "c2": ("c2_dct8_post_sub8_n32_fwd+inv_65536x32x32", 65536, 32, "f32",
+           lambda: _post(32, "dct8"), "c2_inputs", True),
+    "c1": ("c1_dst7_pre_band6_n32_fwd_4096x32x32", 4096, 32, "f64",
+           lambda: _pre(32, "dst7"), "c1_inputs", False),
+}
+for _k in ("dst7", "dct8"):
+    UNIFORM[f"c4_{_k}_pre"] = (f"c4_{_k}_pre_band6_n64_fwd+inv_262144x64x64", 262144, 64, "f32",
+                               (lambda k=_k: _pre(64, k)), "c4_inputs", True)
+    UNIFORM[f"c4_{_k}_post"] = (f"c4_{_k}_post_sub8_n64_fwd+inv_262144x64x64", 262144, 64, "f32",
+                                (lambda k=_k: _post(64, k)), "c4_inputs", True)
+CONFIGS = sorted(UNIFORM) + ["c3_pre", "c3_post", "c5"]
 
 
 # ------------------------------------------------------------------ helpers
@@ -156,66 +156,303 @@ def _peaks():
 def _traffic(workload: str):
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return d.get(workload)
+        return json.loads(p.read_text()).get(workload)
     return None
+
+
+def _block_err(got: np.ndarray, ref: np.ndarray) -> float:
+    n = got.shape[0]
+    num = np.abs(got.astype(np.float64) - ref).reshape(n, -1).max(1)
+    den = np.maximum(np.abs(ref).reshape(n, -1).max(1), 1e-300)
+    return float((num / den).max())
+
+
+# ------------------------------------------------------------------ GPU workloads
+class Workload:
+    """One config on one rank: device buffers, the launches of one step, the
+    oracle gate, and (uniform configs) the host-buffer e2e step."""
+
+    workload = ""
+    dtype = "f32"
+    launches: list = []          # [(name, callable)] per step, in order
+    coef_per_step = 0            # coefficients produced per step (all transforms)
+    bytes_first_launch = 0       # algorithmic bytes of launches[0]
+    e2e = None                   # callable for one end-to-end step, or None
+    e2e_bytes = (0, 0)
+    extra: dict = {}
+
+    def gate(self) -> float:
+        raise NotImplementedError
+
+    def check_e2e(self):
+        pass
+
+
+class Uniform(Workload):
+    def __init__(self, name: str, rank: int):
+        import torch
+        from paper_2505_23618_b200 import _lib, pipeline, workloads
+        wl, nblk, n, dt, make, inputs, inverse = UNIFORM[name]
+        self.workload, self.dtype = wl, dt
+        self.t = make()
+        self.nblk = nblk
+        self.x = getattr(workloads, inputs)("cuda", nblk, offset=rank * nblk)
+        self.y = torch.empty_like(self.x)
+        self.xr = torch.empty_like(self.x)
+        coef = nblk * n * n
+        es = self.x.element_size()
+        self.inverse = inverse
+        self.coef_per_step = coef * (2 if inverse else 1)
+        self.bytes_first_launch = 2 * coef * es
+        lib = _lib.load()
+        ax, self._keep = self.t.axis()
+        self.ax = ax
+        dtc = _lib.F32 if dt == "f32" else _lib.F64
+        st = torch.cuda.current_stream().cuda_stream
+        ref = ctypes.byref(ax)
+
+        def fwd():
+            _lib.check(lib.dctadj_forward_2d(ref, ref, self.x.data_ptr(), self.y.data_ptr(), nblk, dtc, st))
+
+        def inv():
+            _lib.check(lib.dctadj_inverse_2d(ref, ref, self.y.data_ptr(), self.xr.data_ptr(), nblk, dtc, st))
+
+        self.launches = [("forward_2d", fwd)] + ([("inverse_2d", inv)] if inverse else [])
+        # e2e: the same step through the host-buffer entries (pinned arrays)
+        self.xh = self.x.cpu().pin_memory().numpy()
+        self.yh = torch.empty(tuple(self.x.shape), dtype=self.x.dtype).pin_memory().numpy()
+        self.xrh = torch.empty(tuple(self.x.shape), dtype=self.x.dtype).pin_memory().numpy()
+
+        def e2e():
+            pipeline.forward_adjusted_2d_host(self.t, self.t, self.xh, out=self.yh)
+            if inverse:
+                pipeline.inverse_adjusted_2d_host(self.t, self.t, self.yh, out=self.xrh)
+
+        self.e2e = e2e
+        nb = coef * es
+        self.e2e_bytes = (nb * (2 if inverse else 1), nb * (2 if inverse else 1))
+        self.extra = {"blocks_per_gpu": nblk, "block": f"{n}x{n}",
+                      "l2": f"inputs {nb / 1e6:.0f} MB per GPU "
+                            + ("> 126 MB L2; no flush" if nb > 126e6 else "< 126 MB L2: L2-resident")}
+
+    def gate(self):
+        import torch
+        from oracle import oracle as O
+        from paper_2505_23618_b200 import pipeline
+        y0 = pipeline.forward_adjusted_2d(self.t, self.t, self.x)
+        idx = torch.arange(0, self.nblk, max(1, self.nblk // 256), device="cuda")
+        xs = self.x[idx].cpu().numpy().astype(np.float64)
+        ax = _oaxis(self.t)
+        return _block_err(y0[idx].cpu().numpy(), O.adjusted_2d(ax, ax, xs))
+
+    def check_e2e(self):
+        if self.inverse and self.workload.startswith("c2"):
+            if not np.array_equal(np.rint(self.xrh), self.xh):
+                raise SystemExit("e2e round trip lost integer exactness")
+
+
+class Mixed(Workload):
+    """Config 3: 1,048,576 blocks, shapes {16,32}^2 and (h, v) kinds uniform."""
+
+    def __init__(self, side: str, rank: int, nblk: int = 1 << 20):
+        import torch
+        from paper_2505_23618_b200 import _lib, pipeline, workloads
+        self.workload = f"c3_mixed_{side}_fwd+inv_{nblk}blocks"
+        g_h, g_w, kinds = workloads.c3_shapes(nblk, seed=3 + 1000 * rank)
+        h_kind, v_kind = (kinds % 2).numpy(), (kinds // 2).numpy()
+        sizes = np.array([16, 16, 32, 32])
+        h_index = (np.where(g_w.numpy() == 16, 0, 2) + h_kind).astype(np.int32)
+        v_index = (np.where(g_h.numpy() == 16, 0, 2) + v_kind).astype(np.int32)
+        self.batch = pipeline.MixedBatch.packed(h_index, v_index, sizes)
+        if side == "pre":
+            self.table = [_pre(16, "dst7"), _pre(16, "dct8"), _pre(32, "dst7"), _pre(32, "dct8")]
+        else:
+            self.table = [_post(16, "dst7"), _post(16, "dct8"), _post(32, "dst7"), _post(32, "dct8")]
+        # inputs: Laplace-innovation AR(1) blocks, generated per shape and scattered
+        total = self.batch.total_elements
+        self.x = torch.empty(total, device="cuda", dtype=torch.float32)
+        offs = torch.from_numpy(self.batch.offsets).cuda()
+        hh = torch.from_numpy(sizes[v_index]).cuda()
+        ww = torch.from_numpy(sizes[h_index]).cuda()
+        for si, (H, W) in enumerate(((16, 16), (16, 32), (32, 16), (32, 32))):
+            sel = torch.nonzero((hh == H) & (ww == W)).flatten()
+            if sel.numel() == 0:
+                continue
+            blocks = workloads.c3_block(H, W, sel.numel(), seed=3 * 1_000_003 + 97 * rank + si)
+            idx = offs[sel][:, None] + torch.arange(H * W, device="cuda")[None, :]
+            self.x[idx.flatten()] = blocks.reshape(-1)
+            del blocks, idx
+        self.y = torch.empty_like(self.x)
+        self.xr = torch.empty_like(self.x)
+        self.coef_per_step = 2 * total
+        self.bytes_first_launch = 2 * total * 4
+        self.axes = (_lib.Axis * 4)()
+        self._keep = []
+        for k, tr in enumerate(self.table):
+            ax, m = tr.axis()
+            self.axes[k] = ax
+            self._keep.append(m)
+        lib = _lib.load()
+        st = torch.cuda.current_stream().cuda_stream
+        plan = self.batch._plan
+
+        def fwd():
+            _lib.check(lib.dctadj_mixed_forward(plan, self.axes, self.x.data_ptr(), self.y.data_ptr(), 0, st))
+
+        def inv():
+            _lib.check(lib.dctadj_mixed_inverse(plan, self.axes, self.y.data_ptr(), self.xr.data_ptr(), 0, st))
+
+        self.launches = [("mixed_forward", fwd), ("mixed_inverse", inv)]
+        self.h_index, self.v_index = h_index, v_index
+        self.extra = {"blocks_per_gpu": nblk, "coefficients_per_gpu": total,
+                      "classes": int(len(np.unique(h_index * 4 + v_index))),
+                      "l2": f"inputs {total * 4 / 1e6:.0f} MB per GPU > 126 MB L2; no flush"}
+
+    def gate(self):
+        from oracle import oracle as O
+        from paper_2505_23618_b200 import pipeline
+        y = pipeline.mixed_forward(self.batch, self.table, self.x).cpu().numpy()
+        x = self.x.cpu().numpy()
+        worst = 0.0
+        for i in range(0, self.batch.nblk, max(1, self.batch.nblk // 256)):
+            o = int(self.batch.offsets[i])
+            h, w = int(self.batch.sizes[self.v_index[i]]), int(self.batch.sizes[self.h_index[i]])
+            ref = O.adjusted_2d(_oaxis(self.table[self.h_index[i]]), _oaxis(self.table[self.v_index[i]]),
+                                x[o:o + h * w].reshape(1, h, w).astype(np.float64))
+            worst = max(worst, _block_err(y[o:o + h * w].reshape(1, h, w), ref))
+        return worst
+
+
+class Frames(Workload):
+    """Config 5: 64 frames 3840x2160 fp32 per GPU, 32x32 tiles (bottom padded to
+    2176 rows by TMA zero fill); adjusted DST-7 (sub8 post) forward + inverse
+    plus the exact dense DST-7 forward on the same tiles.  The coefficient-
+    domain approximation error sum|Y_adj - Y_exact|^2 / sum|Y_exact|^2 is
+    reported over all tiles and over the 67 unpadded tile rows."""
+
+    def __init__(self, rank: int, world: int, nframes: int = 64):
+        import torch
+        from paper_2505_23618_b200 import _lib, pipeline, shard, workloads
+        from paper_2505_23618_b200.design import (AdjustmentMatrix, Side, SparsityPattern,
+                                                  pattern_schedule_template)
+        from paper_2505_23618_b200.transforms import TransformKind, build_transform
+        f0, f1 = shard.frame_range(rank, world, nframes * world)  # weak scaling: 64 per GPU
+        self.nframes = f1 - f0
+        self.H, self.W = 2160, 3840
+        self.workload = f"c5_frames_{self.nframes}x3840x2160_dst7_post_sub8_fwd+inv+dense_exact"
+        self.frames = workloads.c5_frames(self.nframes, self.H, self.W, offset=f0)
+        self.t = _post(32, "dst7")
+        d7 = build_transform(TransformKind.DST7, 32).entries
+        c = d7 @ build_transform(TransformKind.DCT2, 32).entries.T
+        dense = AdjustmentMatrix(SparsityPattern.dense(32), Side.POST, TransformKind.DCT2,
+                                 TransformKind.DST7, pattern_schedule_template(SparsityPattern.dense(32)), c)
+        self.td = pipeline.make_adjusted_transform(dense)
+        nblk = pipeline.frame_block_count(self.nframes, self.H, self.W, 32, 32)
+        self.y = torch.empty(nblk, 32, 32, device="cuda")
+        self.ye = torch.empty_like(self.y)
+        self.back = torch.empty_like(self.frames)
+        lib = _lib.load()
+        st = torch.cuda.current_stream().cuda_stream
+        (ax, k1), (axd, k2) = self.t.axis(), self.td.axis()
+        self._keep = (ax, k1, axd, k2)
+        r, rd = ctypes.byref(ax), ctypes.byref(axd)
+        F, H, W = self.nframes, self.H, self.W
+
+        def fwd():
+            _lib.check(lib.dctadj_forward_frames(r, r, self.frames.data_ptr(), self.y.data_ptr(), F, H, W, 0, st))
+
+        def inv():
+            _lib.check(lib.dctadj_inverse_frames(r, r, self.y.data_ptr(), self.back.data_ptr(), F, H, W, 0, st))
+
+        def exact():
+            _lib.check(lib.dctadj_forward_frames(rd, rd, self.frames.data_ptr(), self.ye.data_ptr(), F, H, W, 0, st))
+
+        self.launches = [("forward_frames", fwd), ("inverse_frames", inv), ("dense_dst7_frames", exact)]
+        coef = nblk * 1024
+        self.coef_per_step = 3 * coef
+        self.bytes_first_launch = 4 * (F * H * W + coef)
+        self.extra = {"frames_per_gpu": F, "blocks_per_gpu": nblk, "padded_rows": 2176,
+                      "coefficients_padded": coef, "coefficients_unpadded": F * H * W,
+                      "step": "adjusted forward + adjusted inverse + exact dense DST-7 forward "
+                              "(value counts all three transforms)"}
+
+    def gate(self):
+        from oracle import oracle as O
+        from paper_2505_23618_b200 import pipeline
+        y = pipeline.forward_frames(self.t, self.t, self.frames[:1])
+        pad = np.zeros((2176, 3840))
+        pad[:2160] = self.frames[0].cpu().numpy()
+        blocks = pad.reshape(68, 32, 120, 32).transpose(0, 2, 1, 3).reshape(-1, 32, 32)
+        sel = np.arange(0, blocks.shape[0], 37)
+        ax = _oaxis(self.t)
+        return _block_err(y.cpu().numpy()[sel], O.adjusted_2d(ax, ax, blocks[sel]))
+
+    def approximation_error(self):
+        y = self.y.view(self.nframes, 68, 120, 32, 32).double()
+        ye = self.ye.view(self.nframes, 68, 120, 32, 32).double()
+        d_all = (y - ye).pow(2).sum().item()
+        e_all = ye.pow(2).sum().item()
+        d_full = (y[:, :67] - ye[:, :67]).pow(2).sum().item()
+        e_full = ye[:, :67].pow(2).sum().item()
+        return [d_all, e_all, d_full, e_full]
 
 
 # ------------------------------------------------------------------ CPU legs
 def _cpu_worker(args):
     kind, cfg_name, nblk, seed, reps = args
-    import numpy as np  # noqa: F811
     from oracle import oracle as O
-    cfg = CONFIGS[cfg_name]
-    th, tv = cfg["transforms"]()
-    ah, av = _oaxis(th), _oaxis(tv)
+    wl, _, n, _, make, _, inverse = UNIFORM[cfg_name]
+    ax = _oaxis(make())
     rng = np.random.default_rng(seed)
-    x = rng.standard_normal((nblk, cfg["h"], cfg["w"])) * 24.0
+    x = rng.standard_normal((nblk, n, n)) * 24.0
     if kind == "reference":
         ref = O.RefPipeline()
-        fwd = lambda a: ref.forward_2d(ah, av, a)  # noqa: E731
-        inv = lambda a: ref.inverse_2d(ah, av, a)  # noqa: E731
+        fwd = lambda a: ref.forward_2d(ax, ax, a)  # noqa: E731
+        inv = lambda a: ref.inverse_2d(ax, ax, a)  # noqa: E731
     else:
-        fwd = lambda a: O.adjusted_2d(ah, av, a)  # noqa: E731
-        inv = lambda a: O.adjusted_2d(ah, av, a, inverse=True)  # noqa: E731
+        fwd = lambda a: O.adjusted_2d(ax, ax, a)  # noqa: E731
+        inv = lambda a: O.adjusted_2d(ax, ax, a, inverse=True)  # noqa: E731
     t0 = time.perf_counter()
     for _ in range(reps):
         y = fwd(x)
-        if cfg["inverse"]:
+        if inverse:
             inv(y)
     return time.perf_counter() - t0
 
 
-def cpu_throughput(cfg_name: str, seconds: float = 10.0):
+def cpu_throughput(cfg_name: str, seconds: float = 8.0):
     """Reference CPU path on this host's cores: the reference's compiled core
     (oracle/_ref, kind "reference") when built, else the C port (kind "port");
-    one process per core, each on its own contiguous block sample."""
+    one process per core, each on its own block sample, single-threaded BLAS."""
     from multiprocessing import get_context
     from oracle import oracle as O
-    cfg = CONFIGS[cfg_name]
+    if cfg_name not in UNIFORM:
+        cfg_name = "c2"
+    wl, _, n, _, _, _, inverse = UNIFORM[cfg_name]
     kind = "reference" if O.ref_fastcore() is not None else "port"
     cores = O.threads_available()
-    nblk = 256 if cfg["h"] == 32 else 64
-    per_pass = nblk * cfg["h"] * cfg["w"] * (2 if cfg["inverse"] else 1)
-    # calibrate one worker
+    nblk = 256 if n == 32 else 64
+    per_pass = nblk * n * n * (2 if inverse else 1)
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     t1 = _cpu_worker((kind, cfg_name, nblk, 0, 1))
     reps = max(1, int(seconds / max(t1, 1e-6)))
     with get_context("fork").Pool(cores) as pool:
         times = pool.map(_cpu_worker, [(kind, cfg_name, nblk, s, reps) for s in range(cores)])
     value = cores * reps * per_pass / max(times)
-    sample = (f"{cores} processes x {reps} passes x {nblk} blocks ({cfg['h']}x{cfg['w']}, "
-              f"{'fwd+inv' if cfg['inverse'] else 'fwd'}) of the {cfg_name} workload")
+    sample = (f"{cores} processes x {reps} passes x {nblk} blocks ({n}x{n}, "
+              f"{'fwd+inv' if inverse else 'fwd'}) of the {cfg_name} workload")
     return {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
 
 
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
+    cfg = args.config if args.config in UNIFORM else "c2"
+    wl, _, _, dt, _, _, _ = UNIFORM[cfg]
     per = []
     res = None
     for i in range(args.warmup + args.steps):
-        r = cpu_throughput(args.config, seconds=2.0)
+        r = cpu_throughput(cfg, seconds=2.0)
         if i >= args.warmup:
             per.append(r["value"])
             res = r
@@ -223,9 +460,8 @@ def run_reference(args, rank: int, world: int):
     res["value"] = value
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": cfg["workload"], "sample_per_step": res["sample"]},
+            "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "impl": "reference", "config": {"workload": wl, "sample_per_step": res["sample"]},
             "cpu_baseline": res,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -236,60 +472,31 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
 
-    from paper_2505_23618_b200 import pipeline, workloads
-    from paper_2505_23618_b200 import _lib
-
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    cfg = CONFIGS[args.config]
-    th, tv = cfg["transforms"]()
-    nblk = cfg["blocks"]
-    x = getattr(workloads, cfg["inputs"])("cuda", nblk, offset=rank * nblk)
-    y = torch.empty_like(x)
-    xr = torch.empty_like(x)
-    es = x.element_size()
-    coef = nblk * cfg["h"] * cfg["w"]
-
-    # oracle gate before timing (reference benchmark.py:181-190)
-    from oracle import oracle as O
-    y0 = pipeline.forward_adjusted_2d(th, tv, x)
-    idx = torch.arange(0, nblk, max(1, nblk // 256), device="cuda")
-    xs = x[idx].cpu().numpy().astype(np.float64)
-    ys = O.adjusted_2d(_oaxis(th), _oaxis(tv), xs)
-    err = float((np.abs(y0[idx].cpu().numpy() - ys).reshape(len(idx), -1).max(1)
-                 / np.maximum(np.abs(ys).reshape(len(idx), -1).max(1), 1e-300)).max())
-    tol = 1e-5 if cfg["dtype"] == "f32" else 1e-9
-    if err > tol:
-        raise SystemExit(f"oracle gate failed: rel err {err:.3e} > {tol}")
-    del y0
-
-    stream = torch.cuda.current_stream()
-
-    def step():
-        _fwd(x, y)
-        if cfg["inverse"]:
-            _inv(y, xr)
-
-    import ctypes
-    (axh, keep_h), (axv, keep_v) = th.axis(), tv.axis()
-    dt = _lib.F32 if x.dtype == torch.float32 else _lib.F64
-    lib = _lib.load()
-
-    def _fwd(a, b):
-        _lib.check(lib.dctadj_forward_2d(ctypes.byref(axh), ctypes.byref(axv), a.data_ptr(),
-                                         b.data_ptr(), nblk, dt, stream.cuda_stream))
-
-    def _inv(a, b):
-        _lib.check(lib.dctadj_inverse_2d(ctypes.byref(axh), ctypes.byref(axv), a.data_ptr(),
-                                         b.data_ptr(), nblk, dt, stream.cuda_stream))
-
-    for _ in range(args.warmup):
-        step()
+    if args.config in UNIFORM:
+        w = Uniform(args.config, rank)
+    elif args.config.startswith("c3"):
+        w = Mixed(args.config.split("_")[1], rank)
+    else:
+        w = Frames(rank, world)
     torch.cuda.synchronize()
 
-    n_ev = 3 if cfg["inverse"] else 2
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    # oracle gate before timing (reference benchmark.py:181-190)
+    err = w.gate()
+    tol = 1e-5 if w.dtype == "f32" else 1e-9
+    if err > tol:
+        raise SystemExit(f"oracle gate failed: rel err {err:.3e} > {tol}")
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for _, fn in w.launches:
+            fn()
+    torch.cuda.synchronize()
+
+    nl = len(w.launches)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
     with ClockSampler(torch.cuda.current_device()) as clk:
         if world > 1:
             dist.barrier()
@@ -297,74 +504,68 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         clk.mark_start()
         for k in range(args.steps):
             evs[k][0].record(stream)
-            _fwd(x, y)
-            evs[k][1].record(stream)
-            if cfg["inverse"]:
-                _inv(y, xr)
-                evs[k][2].record(stream)
+            for j, (_, fn) in enumerate(w.launches):
+                fn()
+                evs[k][j + 1].record(stream)
         torch.cuda.synchronize()
         clk.mark_end()
         if world > 1:
             dist.barrier()
-    fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    inv_ms = [e[1].elapsed_time(e[2]) for e in evs] if cfg["inverse"] else []
+    per_launch_ms = [float(np.mean([e[j].elapsed_time(e[j + 1]) for e in evs])) for j in range(nl)]
     total_ms = evs[0][0].elapsed_time(evs[-1][-1])
 
-    # e2e through the host-buffer C-ABI entries (pinned host memory, copies inside)
-    xh = x.cpu().pin_memory()
-    yh = torch.empty_like(xh).pin_memory()
-    xrh = torch.empty_like(xh).pin_memory()
-    xh_np, yh_np, xrh_np = xh.numpy(), yh.numpy(), xrh.numpy()
-    e2e_steps = max(2, min(args.steps, 5))
-    for _ in range(1):
-        pipeline.forward_adjusted_2d_host(th, tv, xh_np, out=yh_np)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        pipeline.forward_adjusted_2d_host(th, tv, xh_np, out=yh_np)
-        if cfg["inverse"]:
-            pipeline.inverse_adjusted_2d_host(th, tv, yh_np, out=xrh_np)
-    e2e_s = time.perf_counter() - t0
-    if cfg["inverse"] and not np.array_equal(np.rint(xrh_np), xh_np) and cfg["inputs"] == "c2_inputs":
-        raise SystemExit("e2e round trip lost integer exactness")
+    e2e_s = None
+    if w.e2e is not None:
+        w.e2e()  # warm
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e2e_steps = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            w.e2e()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        w.check_e2e()
+
+    approx = w.approximation_error() if isinstance(w, Frames) else None
 
     if world > 1:
-        t = torch.tensor([total_ms, e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_ms, e2e_s or 0.0], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_s = float(t[0]), float(t[1])
+        total_ms, e2e_s = float(t[0]), (float(t[1]) if e2e_s is not None else None)
+        if approx is not None:
+            a = torch.tensor(approx, device="cuda", dtype=torch.float64)
+            dist.all_reduce(a, op=dist.ReduceOp.SUM)
+            approx = a.tolist()
 
-    per_step_coef = coef * (2 if cfg["inverse"] else 1)
     ms_per_step = total_ms / args.steps
-    value = world * per_step_coef / (ms_per_step / 1e3)
-    e2e_value = world * per_step_coef * e2e_steps / e2e_s
-    bytes_per_launch = 2 * coef * es  # read x once, write y once
-    fwd_avg = float(np.mean(fwd_ms))
+    value = world * w.coef_per_step / (ms_per_step / 1e3)
     peak, peak_src = _peaks()
-    achieved = bytes_per_launch / (fwd_avg / 1e3) / 1e9
-    traffic = _traffic(cfg["workload"])
+    achieved = w.bytes_first_launch / (per_launch_ms[0] / 1e3) / 1e9
+    config = {"workload": w.workload, "parallelism": f"block-range shards x{world}",
+              "oracle_gate_rel_err": err}
+    config.update(w.extra)
+    if approx is not None:
+        config["approx_error_vs_exact_dst7_all_tiles"] = approx[0] / approx[1]
+        config["approx_error_vs_exact_dst7_unpadded_tile_rows"] = approx[2] / approx[3]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
-        "data": "synthetic (seeded AR(1) residual blocks, SURVEY.md App. A D12)",
-        "config": {"workload": cfg["workload"], "blocks_per_gpu": nblk,
-                   "block": f"{cfg['h']}x{cfg['w']}",
-                   "l2": f"inputs {coef * es / 1e6:.0f} MB per GPU > 126 MB L2; no flush",
-                   "parallelism": f"block-range shards x{world}",
-                   "oracle_gate_rel_err": err},
+        "scaling": "weak", "vs_baseline": None, "dtype": w.dtype,
+        "data": "synthetic (seeded residual fields per BASELINE.json configs, SURVEY.md App. A D12)",
+        "config": config,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "tile_kernel forward (fused rows+cols+adjustment)",
-                     "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "avg_launch_ms": fwd_avg,
-                     "inverse_avg_launch_ms": float(np.mean(inv_ms)) if inv_ms else None},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step":
-                coef * es * (2 if cfg["inverse"] else 1),
-                "d2h_bytes_per_step": coef * es * (2 if cfg["inverse"] else 1),
-                "api": "forward_adjusted_2d_host / inverse_adjusted_2d_host (C-ABI *_2d_host)"},
-        "gpu_launches": args.steps * (2 if cfg["inverse"] else 1),
+                     "frac": achieved / peak, "traffic": _traffic(w.workload),
+                     "peak_source": peak_src,
+                     "kernel": f"tile_kernel ({w.launches[0][0]})",
+                     "algorithmic_bytes_per_launch": w.bytes_first_launch,
+                     "avg_launch_ms": per_launch_ms[0],
+                     "per_launch_ms": dict(zip([n for n, _ in w.launches], per_launch_ms))},
+        "e2e": ({"value": world * w.coef_per_step / e2e_s, "unit": UNIT,
+                 "h2d_bytes_per_step": w.e2e_bytes[0], "d2h_bytes_per_step": w.e2e_bytes[1],
+                 "api": "forward_adjusted_2d_host / inverse_adjusted_2d_host (C-ABI *_2d_host)"}
+                if e2e_s else None),
+        "gpu_launches": args.steps * nl,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -380,7 +581,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=CONFIGS)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)

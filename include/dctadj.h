@@ -120,6 +120,24 @@ int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void
                           void* frames, int32_t nframes, int32_t height, int32_t width,
                           int32_t dtype, void* stream);
 
+/* ---- mixed-shape batches (config 3): blocks of different sizes packed back
+ * to back in one buffer of `total_elements` samples.  Block i starts at element
+ * offsets[i] (a multiple of its width), its rows use axis-table entry
+ * h_index[i] (width = sizes[h_index[i]]) and its columns entry v_index[i]
+ * (height = sizes[v_index[i]]).  The plan buckets blocks by (h, v) class once
+ * (host arrays in, device offset lists kept); each call then runs one gather
+ * kernel per class.  `table` (ntable entries, sizes as in the plan) is read per
+ * call, so the same plan serves pre- and post-adjusted runs. */
+typedef struct dctadj_mixed dctadj_mixed;
+int dctadj_mixed_create(const int64_t* offsets, const int32_t* h_index, const int32_t* v_index,
+                        int64_t nblk, const int32_t* sizes, int32_t ntable,
+                        int64_t total_elements, dctadj_mixed** plan);
+int dctadj_mixed_forward(const dctadj_mixed* plan, const dctadj_axis* table, const void* x,
+                         void* y, int32_t dtype, void* stream);
+int dctadj_mixed_inverse(const dctadj_mixed* plan, const dctadj_axis* table, const void* y,
+                         void* x, int32_t dtype, void* stream);
+int dctadj_mixed_destroy(dctadj_mixed* plan);
+
 /* ---- diagnostics ---- */
 /* The tile pipeline with no arithmetic (TMA load -> smem -> TMA store) on
  * (nblk, h, w) blocks, h x w in {32x32, 64x64, 16x16}: the data-movement

@@ -502,6 +502,65 @@ static int run_frames(const dctadj_axis* h, const dctadj_axis* v, const void* in
                 inverse ? MODE_FRAME : MODE_LINEAR, nframes, height, width, st);
 }
 
+// ------------------------------------------------------------- mixed batches
+}  // namespace dctadj
+
+struct dctadj_mixed {
+  struct Class {
+    int32_t h_index, v_index;
+    int64_t count;
+    int64_t* offsets;  // device, into `all`
+  };
+  std::vector<Class> classes;
+  std::vector<int32_t> sizes;
+  int64_t total_elements = 0;
+  int64_t nblk = 0;
+  int64_t* all = nullptr;  // device
+  int device = 0;
+};
+
+namespace dctadj {
+
+static int run_mixed(const dctadj_mixed* plan, const dctadj_axis* table, const void* x, void* y,
+                     int dtype, bool inverse, cudaStream_t st) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if (!plan || !table) return fail(ST_ERR_VALUE, "NULL plan or axis table");
+  for (size_t k = 0; k < plan->sizes.size(); ++k) {
+    if ((rc = validate_axis(&table[k])) != ST_OK) return rc;
+    if (table[k].n != plan->sizes[k])
+      return fail(ST_ERR_SHAPE, "axis table entry %zu has n=%d, plan built for %d", k,
+                  table[k].n, plan->sizes[k]);
+  }
+  if (plan->nblk == 0) return ST_OK;
+  if (!x || !y) return fail(ST_ERR_VALUE, "NULL data pointer");
+  for (const auto& c : plan->classes) {
+    const dctadj_axis* h = &table[c.h_index];
+    const dctadj_axis* v = &table[c.v_index];
+    AxisPlan ph, pv;
+    if ((rc = plan_axis(h, inverse, false, &ph)) || (rc = plan_axis(v, inverse, false, &pv))) return rc;
+    Launch L;
+    rc = prepare(L, ph, &pv, dtype, v->n, h->n, inverse, MODE_GATHER, MODE_GATHER, st);
+    if (rc == ST_ERR_UNSUPPORTED) {
+      if ((rc = plan_axis(h, inverse, true, &ph)) || (rc = plan_axis(v, inverse, true, &pv))) return rc;
+      L = Launch();
+      rc = prepare(L, ph, &pv, dtype, v->n, h->n, inverse, MODE_GATHER, MODE_GATHER, st);
+      if (rc == ST_ERR_UNSUPPORTED)
+        return fail(rc, "no gather kernel for %dx%d blocks, dtype %d", v->n, h->n, dtype);
+    }
+    if (rc) return rc;
+    L.a.in = x;
+    L.a.out = y;
+    L.a.rows = plan->total_elements / h->n;
+    L.a.offsets = c.offsets;
+    L.a.gather_blocks = c.count;
+    rc = L.k->fn(L.a);
+    int rc2 = finish(L, st);
+    if (rc || rc2) return rc ? rc : rc2;
+  }
+  return ST_OK;
+}
+
 // generic rectangular dense product (rows != n), the one path off the tile kernel
 template <typename T>
 __global__ void dense_rect_kernel(const T* __restrict__ m, int rows, const T* __restrict__ x,
@@ -679,6 +738,78 @@ int dctadj_copy_tiles(const void* x, void* y, int64_t nblk, int32_t h, int32_t w
   L.a.out = y;
   L.a.rows = nblk * h;
   return L.k->fn(L.a);
+}
+
+int dctadj_mixed_create(const int64_t* offsets, const int32_t* h_index, const int32_t* v_index,
+                        int64_t nblk, const int32_t* sizes, int32_t ntable,
+                        int64_t total_elements, dctadj_mixed** out) {
+  if (!out) return fail(ST_ERR_VALUE, "NULL plan output");
+  *out = nullptr;
+  if (nblk < 0 || ntable < 1 || total_elements < 0)
+    return fail(ST_ERR_SHAPE, "bad mixed batch geometry");
+  if (nblk > 0 && (!offsets || !h_index || !v_index || !sizes))
+    return fail(ST_ERR_VALUE, "NULL descriptor array");
+  for (int k = 0; k < ntable; ++k)
+    if (!fast_size(sizes[k]))
+      return fail(ST_ERR_DIMENSION, "fast transforms support sizes (4, 8, 16, 32, 64), got %d",
+                  sizes[k]);
+  // bucket by (h, v) class: counting sort on the host, once
+  std::vector<int64_t> count(static_cast<size_t>(ntable) * ntable, 0);
+  for (int64_t i = 0; i < nblk; ++i) {
+    const int hi = h_index[i], vi = v_index[i];
+    if (hi < 0 || hi >= ntable || vi < 0 || vi >= ntable)
+      return fail(ST_ERR_VALUE, "block %lld: axis index out of range", (long long)i);
+    const int64_t w = sizes[hi], hgt = sizes[vi];
+    if (offsets[i] < 0 || offsets[i] % w != 0 || offsets[i] + hgt * w > total_elements)
+      return fail(ST_ERR_SHAPE, "block %lld: offset %lld does not fit a %lldx%lld block in %lld elements",
+                  (long long)i, (long long)offsets[i], (long long)hgt, (long long)w,
+                  (long long)total_elements);
+    if (total_elements % w != 0)
+      return fail(ST_ERR_SHAPE, "buffer of %lld elements is not a whole number of %lld-wide rows",
+                  (long long)total_elements, (long long)w);
+    ++count[hi * ntable + vi];
+  }
+  auto* plan = new dctadj_mixed();
+  plan->sizes.assign(sizes, sizes + ntable);
+  plan->total_elements = total_elements;
+  plan->nblk = nblk;
+  cudaGetDevice(&plan->device);
+  std::vector<int64_t> start(count.size() + 1, 0);
+  for (size_t c = 0; c < count.size(); ++c) start[c + 1] = start[c] + count[c];
+  std::vector<int64_t> sorted(static_cast<size_t>(nblk));
+  std::vector<int64_t> fill(start.begin(), start.end() - 1);
+  for (int64_t i = 0; i < nblk; ++i) sorted[fill[h_index[i] * ntable + v_index[i]]++] = offsets[i];
+  if (nblk > 0) {
+    if (cudaMalloc(&plan->all, sizeof(int64_t) * nblk) != cudaSuccess ||
+        cudaMemcpy(plan->all, sorted.data(), sizeof(int64_t) * nblk, cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+      cudaFree(plan->all);
+      delete plan;
+      return fail(ST_ERR_CUDA, "mixed plan upload: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  for (int hi = 0; hi < ntable; ++hi)
+    for (int vi = 0; vi < ntable; ++vi) {
+      const size_t c = static_cast<size_t>(hi) * ntable + vi;
+      if (count[c]) plan->classes.push_back({hi, vi, count[c], plan->all + start[c]});
+    }
+  *out = plan;
+  return ST_OK;
+}
+
+int dctadj_mixed_forward(const dctadj_mixed* plan, const dctadj_axis* table, const void* x,
+                         void* y, int32_t dtype, void* stream) {
+  return run_mixed(plan, table, x, y, dtype, false, S(stream));
+}
+int dctadj_mixed_inverse(const dctadj_mixed* plan, const dctadj_axis* table, const void* y,
+                         void* x, int32_t dtype, void* stream) {
+  return run_mixed(plan, table, y, x, dtype, true, S(stream));
+}
+int dctadj_mixed_destroy(dctadj_mixed* plan) {
+  if (!plan) return ST_OK;
+  if (plan->all) cudaFree(plan->all);
+  delete plan;
+  return ST_OK;
 }
 
 const char* dctadj_status_string(int32_t status) {

@@ -25,6 +25,10 @@ struct LaunchArgs {
   const void* col_coef = nullptr;  // host, packed AxisOp::Coef of the column op
   const void* dense_row = nullptr; // device, W x W (row op ST_DENSE)
   const void* dense_col = nullptr; // device, H x H (column op ST_DENSE)
+  // GATHER side: `gather_blocks` blocks at element offsets `offsets` (device)
+  // of a packed buffer of `rows` x W elements
+  const int64_t* offsets = nullptr;
+  int64_t gather_blocks = 0;
   cudaStream_t stream = nullptr;
 };
 
@@ -52,10 +56,11 @@ template <typename T, int H, int W, int P, int MODE>
 int make_map(CUtensorMap* map, const void* base, const LaunchArgs& a) {
   using L = TileLayout<T, H, W, P>;
   constexpr int dt = sizeof(T) == 4 ? DT_F32 : DT_F64;
-  if constexpr (MODE == MODE_LINEAR) {
+  if constexpr (MODE == MODE_LINEAR || MODE == MODE_GATHER) {
     uint64_t dims[2] = {static_cast<uint64_t>(W), static_cast<uint64_t>(a.rows)};
     uint64_t strides[1] = {static_cast<uint64_t>(W) * sizeof(T)};
-    uint32_t box[2] = {static_cast<uint32_t>(L::BW), static_cast<uint32_t>(L::PH)};
+    uint32_t box[2] = {static_cast<uint32_t>(L::BW),
+                       static_cast<uint32_t>(MODE == MODE_GATHER ? H : L::PH)};
     return encode_tensor_map(map, dt, 2, dims, strides, box, L::BRB, const_cast<void*>(base));
   } else {
     uint64_t dims[3] = {static_cast<uint64_t>(a.frame_w), static_cast<uint64_t>(a.frame_h),
@@ -81,6 +86,10 @@ int launch_tile(const LaunchArgs& a) {
     g.tiles_x = a.frame_w / W;
     g.nblocks = static_cast<int64_t>(a.frames) * g.tiles_y * g.tiles_x;
     g.ntiles = (g.nblocks + P - 1) / P;
+  } else if (IN_MODE == MODE_GATHER) {
+    g.nblocks = a.gather_blocks;
+    g.ntiles = (g.nblocks + P - 1) / P;
+    g.offsets = a.offsets;
   } else {
     g.ntiles = (a.rows + L::PH - 1) / L::PH;
     g.nblocks = g.ntiles * P;

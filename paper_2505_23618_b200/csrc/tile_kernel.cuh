@@ -139,7 +139,11 @@ struct TileLayout {
   }
 };
 
-enum Mode : int { MODE_LINEAR = 0, MODE_FRAME = 1 };
+// LINEAR: super-tile t = rows [t*P*H, (t+1)*P*H) of a [rows, W] view.
+// FRAME:  blocks in raster order of (F, height, width) frames.
+// GATHER: block i of a class list sits at element offset offsets[i] of a packed
+//         mixed-shape buffer viewed as [elements / W, W] (config 3).
+enum Mode : int { MODE_LINEAR = 0, MODE_FRAME = 1, MODE_GATHER = 2 };
 
 struct Geom {
   int64_t ntiles;      // super-tiles
@@ -148,6 +152,7 @@ struct Geom {
   int32_t tiles_x;     // FRAME: tile columns per frame
   const void* dense_row;  // device N x N (T) for ST_DENSE row op
   const void* dense_col;  // device N x N (T) for ST_DENSE column op
+  const int64_t* offsets; // GATHER: element offset of each block (device)
 };
 
 template <typename T, int W, int H, int RC, int CC>
@@ -156,10 +161,27 @@ struct KParams {
   typename AxisOp<T, H, CC>::Coef col;
 };
 
+// GATHER: lane p < nb moves block p of the super-tile (element offset `off`).
+template <typename T, int H, int W, int P>
+DA_DEV void gather_io(bool load, void* stage, const CUtensorMap* map, uint64_t* bar, int lane,
+                      int nb, int64_t off) {
+  using L = TileLayout<T, H, W, P>;
+  if (lane >= nb) return;
+  const int row0 = static_cast<int>(off / W);
+#pragma unroll
+  for (int b = 0; b < L::NB; ++b) {
+    uint8_t* d = static_cast<uint8_t*>(stage) + b * L::BOXB + lane * H * L::BRB;
+    if (load)
+      tma_load_2d(d, map, bar, b * L::BW, row0);
+    else
+      tma_store_2d(map, d, b * L::BW, row0);
+  }
+}
+
 // Blocks of super-tile t that exist (a FRAME super-tile may be cut short).
 template <int P, int MODE>
 DA_DEV int tile_blocks(int64_t t, const Geom& g) {
-  if constexpr (MODE == MODE_LINEAR || P == 1) {
+  if constexpr (MODE == MODE_LINEAR) {
     return P;
   } else {
     const int64_t left = g.nblocks - t * P;
@@ -372,16 +394,43 @@ __global__ void __launch_bounds__(NG * 32)
   const int64_t gstride = static_cast<int64_t>(gridDim.x) * NG;
   const int64_t ntiles = geom.ntiles;
 
-  if (lane == 0) {
+  constexpr bool GATHER = IN_MODE == MODE_GATHER;
+  static_assert(GATHER == (OUT_MODE == MODE_GATHER), "gather mode is in+out");
+  static_assert(!GATHER || P <= 32, "one lane per gathered block");
+  // GATHER: the offsets of the blocks in flight (stage-major) and a register
+  // prefetch of the next refill's offsets, one lane per block
+  __shared__ int64_t goffs[GATHER ? NG * S * P : 1];
+  int64_t* my_offs = goffs + (GATHER ? warp * S * P : 0);
+  int64_t pref = 0;
+
+  if constexpr (!GATHER) {
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int64_t t = gid + s * gstride;
+        if (t < ntiles) {
+          const int nb = tile_blocks<P, IN_MODE>(t, geom);
+          mbar_arrive_expect_tx(&bars[s], L::TILEB / P * nb);
+          issue_tile_io<T, H, W, P, IN_MODE, CH>(true, ring + s * L::STAGEB, &in_map, &bars[s], t,
+                                                 geom, nb);
+        }
+      }
+    }
+  } else {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int64_t t = gid + s * gstride;
       if (t < ntiles) {
         const int nb = tile_blocks<P, IN_MODE>(t, geom);
-        mbar_arrive_expect_tx(&bars[s], L::TILEB / P * nb);
-        issue_tile_io<T, H, W, P, IN_MODE, CH>(true, ring + s * L::STAGEB, &in_map, &bars[s], t, geom, nb);
+        if (lane == 0) mbar_arrive_expect_tx(&bars[s], L::TILEB / P * nb);
+        __syncwarp();
+        const int64_t off = lane < nb ? geom.offsets[t * P + lane] : 0;
+        if (lane < P) my_offs[s * P + lane] = off;
+        gather_io<T, H, W, P>(true, ring + s * L::STAGEB, &in_map, &bars[s], lane, nb, off);
       }
     }
+    const int64_t tp = gid + S * gstride;
+    if (tp < ntiles && lane < tile_blocks<P, IN_MODE>(tp, geom)) pref = geom.offsets[tp * P + lane];
   }
 
   int s = 0;
@@ -408,20 +457,42 @@ __global__ void __launch_bounds__(NG * 32)
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
-      issue_tile_io<T, H, W, P, OUT_MODE, CH>(false, buf, &out_map, nullptr, t, geom,
-                                          tile_blocks<P, OUT_MODE>(t, geom));
+    if constexpr (!GATHER) {
+      if (lane == 0) {
+        issue_tile_io<T, H, W, P, OUT_MODE, CH>(false, buf, &out_map, nullptr, t, geom,
+                                                tile_blocks<P, OUT_MODE>(t, geom));
+        bulk_commit();
+        // refill the stage freed by the previous tile with the tile S-1 strides ahead
+        if (k >= 1) {
+          const int64_t tn = t + (S - 1) * gstride;
+          if (tn < ntiles) {
+            const int sp = (s == 0) ? S - 1 : s - 1;
+            bulk_wait_read<1>();
+            const int nb = tile_blocks<P, IN_MODE>(tn, geom);
+            mbar_arrive_expect_tx(&bars[sp], L::TILEB / P * nb);
+            issue_tile_io<T, H, W, P, IN_MODE, CH>(true, ring + sp * L::STAGEB, &in_map, &bars[sp],
+                                                   tn, geom, nb);
+          }
+        }
+      }
+    } else {
+      const int nbt = tile_blocks<P, OUT_MODE>(t, geom);
+      gather_io<T, H, W, P>(false, buf, &out_map, nullptr, lane, nbt,
+                            lane < P ? my_offs[s * P + lane] : 0);
       bulk_commit();
-      // refill the stage freed by the previous tile with the tile S-1 strides ahead
       if (k >= 1) {
         const int64_t tn = t + (S - 1) * gstride;
         if (tn < ntiles) {
           const int sp = (s == 0) ? S - 1 : s - 1;
           bulk_wait_read<1>();
           const int nb = tile_blocks<P, IN_MODE>(tn, geom);
-          mbar_arrive_expect_tx(&bars[sp], L::TILEB / P * nb);
-          issue_tile_io<T, H, W, P, IN_MODE, CH>(true, ring + sp * L::STAGEB, &in_map, &bars[sp], tn,
-                                             geom, nb);
+          if (lane == 0) mbar_arrive_expect_tx(&bars[sp], L::TILEB / P * nb);
+          __syncwarp();
+          if (lane < P) my_offs[sp * P + lane] = pref;
+          gather_io<T, H, W, P>(true, ring + sp * L::STAGEB, &in_map, &bars[sp], lane, nb, pref);
+          const int64_t tq = tn + gstride;  // prefetch the next refill's offsets
+          pref = (tq < ntiles && lane < tile_blocks<P, IN_MODE>(tq, geom))
+                     ? geom.offsets[tq * P + lane] : 0;
         }
       }
     }
@@ -431,7 +502,7 @@ __global__ void __launch_bounds__(NG * 32)
       phase ^= 1;
     }
   }
-  if (lane == 0) bulk_wait_all();
+  if (GATHER || lane == 0) bulk_wait_all();
 }
 
 }  // namespace dctadj

@@ -15,6 +15,7 @@ round trip) behind the C-ABI.  New entries:
                                               pipeline.py:236-239), one kernel
   forward_frames / inverse_frames             whole frames tiled into blocks
   forward_adjusted_2d_host / ..._host         host buffers, pipelined copies
+  MixedBatch / mixed_forward / mixed_inverse  packed mixed-shape batches (config 3)
 Extension: base DCT-3 is accepted (the DCT-8 pre-adjustment, SURVEY.md App. A
 D3, built with design.flip_pre_adjustment); the reference raises
 ConfigurationError for it.
@@ -277,3 +278,81 @@ def inverse_frames(th: AdjustedTransform, tv: AdjustedTransform, coefs, height: 
     _lib.call("dctadj_inverse_frames", ctypes.byref(axh), ctypes.byref(axv), t.data_ptr(),
               y.data_ptr(), f, height, width, _device.dtype_code(t), _device.stream_handle())
     return _device.from_device(y, as_np)
+
+
+# ---------------------------------------------------------------- mixed batches
+class MixedBatch:
+    """Blocks of different shapes packed back to back in one buffer (config 3).
+
+    Block i occupies heights[i] x widths[i] samples starting at element
+    `offsets[i]`; its rows use table entry h_index[i] and its columns entry
+    v_index[i] of the AdjustedTransform table passed to mixed_forward /
+    mixed_inverse (sizes fixed here).  The blocks are bucketed by (h, v) class
+    once, in the C-ABI plan (dctadj_mixed_create); every call is then one
+    gather kernel per class.
+    """
+
+    def __init__(self, offsets, h_index, v_index, sizes, total_elements: int):
+        _device.require_cuda()
+        self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        self.h_index = np.ascontiguousarray(h_index, dtype=np.int32)
+        self.v_index = np.ascontiguousarray(v_index, dtype=np.int32)
+        self.sizes = np.ascontiguousarray(sizes, dtype=np.int32)
+        self.total_elements = int(total_elements)
+        n = self.offsets.shape[0]
+        if not (self.h_index.shape[0] == self.v_index.shape[0] == n):
+            raise ShapeError("offsets, h_index and v_index must have one entry per block")
+        self._plan = ctypes.c_void_p()
+        _lib.call("dctadj_mixed_create", self.offsets.ctypes.data, self.h_index.ctypes.data,
+                  self.v_index.ctypes.data, n, self.sizes.ctypes.data, len(self.sizes),
+                  self.total_elements, ctypes.byref(self._plan))
+
+    @staticmethod
+    def packed(h_index, v_index, sizes) -> "MixedBatch":
+        """Pack blocks contiguously in the given order."""
+        sizes = np.asarray(sizes, dtype=np.int64)
+        areas = sizes[np.asarray(h_index)] * sizes[np.asarray(v_index)]
+        offsets = np.concatenate([[0], np.cumsum(areas)[:-1]]) if len(areas) else np.zeros(0, np.int64)
+        return MixedBatch(offsets, h_index, v_index, sizes, int(areas.sum()))
+
+    @property
+    def nblk(self) -> int:
+        return int(self.offsets.shape[0])
+
+    def block_slices(self):
+        """(offset, H, W) per block (host-side view helper)."""
+        for o, hi, vi in zip(self.offsets, self.h_index, self.v_index):
+            yield int(o), int(self.sizes[vi]), int(self.sizes[hi])
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and plan.value and _lib._lib is not None:
+            _lib._lib.dctadj_mixed_destroy(plan)
+            self._plan = None
+
+
+def _mixed(fn: str, batch: MixedBatch, table, x):
+    t, as_np = _device.to_device(x)
+    if t.dim() != 1 or t.shape[0] != batch.total_elements:
+        raise ShapeError(f"expected a packed buffer of {batch.total_elements} samples")
+    if len(table) != len(batch.sizes):
+        raise ShapeError(f"table has {len(table)} entries, plan expects {len(batch.sizes)}")
+    axes = (_lib.Axis * len(table))()
+    keep = []
+    for k, tr in enumerate(table):
+        ax, m = tr.axis()
+        axes[k] = ax
+        keep.append(m)
+    y = _device.empty_like(t)
+    _lib.call(fn, batch._plan, axes, t.data_ptr(), y.data_ptr(), _device.dtype_code(t),
+              _device.stream_handle())
+    return _device.from_device(y, as_np)
+
+
+def mixed_forward(batch: MixedBatch, table, x):
+    """Forward adjusted 2-D transform of every block of a packed mixed batch."""
+    return _mixed("dctadj_mixed_forward", batch, table, x)
+
+
+def mixed_inverse(batch: MixedBatch, table, y):
+    return _mixed("dctadj_mixed_inverse", batch, table, y)

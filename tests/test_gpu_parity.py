@@ -334,3 +334,61 @@ def test_large_batch_properties():
     xs = x[idx].cpu().numpy().astype(np.float64)
     ax = oaxis(t.adjustment)
     assert rel_err(y[idx].cpu().numpy(), O.adjusted_2d(ax, ax, xs)) < F32_TOL
+
+
+# ---------------------------------------------------------------- mixed batches (C3)
+def _c3_table(side):
+    from paper_2505_23618_b200.design import dct8_adjustment_from_dst7 as d8
+    tab = []
+    for n in (16, 32):
+        if side == "pre":
+            a = matio.load_designed(f"band6_pre_dst3_dst7_n{n}")
+            tab += [a, flip_pre_adjustment(a)]
+        else:
+            a = matio.load_designed(f"sub8_post_dct2_dst7_n{n}")
+            tab += [a, d8(a)]
+    return [pipeline.make_adjusted_transform(a) for a in tab]  # [16/dst7, 16/dct8, 32/dst7, 32/dct8]
+
+
+@pytest.mark.parametrize("side", ["pre", "post"])
+@pytest.mark.parametrize("nblk", [1, 7, 301])
+def test_mixed_batch_matches_oracle(side, nblk):
+    rng = np.random.default_rng(nblk)
+    h_index = rng.integers(0, 4, nblk)
+    v_index = rng.integers(0, 4, nblk)
+    batch = pipeline.MixedBatch.packed(h_index, v_index, [16, 16, 32, 32])
+    table = _c3_table(side)
+    x = rng.standard_normal(batch.total_elements).astype(np.float32) * 20
+    y = pipeline.mixed_forward(batch, table, dev(x)).cpu().numpy()
+    xr = pipeline.mixed_inverse(batch, table, dev(y)).cpu().numpy()
+    for (o, h, w), hi, vi in zip(batch.block_slices(), h_index, v_index):
+        blk = x[o:o + h * w].reshape(1, h, w).astype(np.float64)
+        ref = O.adjusted_2d(oaxis(table[hi].adjustment), oaxis(table[vi].adjustment), blk)
+        assert rel_err(y[o:o + h * w].reshape(1, h, w), ref) < F32_TOL
+        assert rel_err(xr[o:o + h * w].reshape(1, h, w), blk) < F32_TOL
+
+
+def test_mixed_batch_shuffled_offsets_and_errors():
+    rng = np.random.default_rng(3)
+    nblk = 64
+    h_index = rng.integers(0, 4, nblk)
+    v_index = rng.integers(0, 4, nblk)
+    sizes = np.array([16, 16, 32, 32])
+    areas = sizes[h_index] * sizes[v_index]
+    order = rng.permutation(nblk)                      # blocks stored out of order
+    offs = np.zeros(nblk, np.int64)
+    offs[order] = np.concatenate([[0], np.cumsum(areas[order])[:-1]])
+    batch = pipeline.MixedBatch(offs, h_index, v_index, sizes, int(areas.sum()))
+    table = _c3_table("post")
+    x = rng.standard_normal(batch.total_elements).astype(np.float32)
+    y = pipeline.mixed_forward(batch, table, dev(x)).cpu().numpy()
+    for (o, h, w), hi, vi in zip(batch.block_slices(), h_index, v_index):
+        ref = O.adjusted_2d(oaxis(table[hi].adjustment), oaxis(table[vi].adjustment),
+                            x[o:o + h * w].reshape(1, h, w).astype(np.float64))
+        assert rel_err(y[o:o + h * w].reshape(1, h, w), ref) < F32_TOL
+    with pytest.raises(ShapeError):
+        pipeline.MixedBatch([8], [2], [2], sizes, 4096)        # offset not a multiple of W
+    with pytest.raises(ShapeError):
+        pipeline.MixedBatch([0], [2], [2], sizes, 512)         # block overruns the buffer
+    with pytest.raises(ShapeError):
+        pipeline.mixed_forward(batch, table[:2], dev(x))

@@ -11,10 +11,10 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2505_23618_b200 import _lib, workloads  # noqa: E402
 
-cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
-th, tv = cfg["transforms"]()
-nblk = cfg["blocks"]
-x = getattr(workloads, cfg["inputs"])("cuda", nblk)
+wl, nblk, n_, dt_, make, inputs, inverse = bench.UNIFORM[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+cfg = {"h": n_, "w": n_}
+th = tv = make()
+x = getattr(workloads, inputs)("cuda", nblk)
 y = torch.empty_like(x)
 xr = torch.empty_like(x)
 lib = _lib.load()

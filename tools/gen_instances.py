@@ -126,6 +126,13 @@ def instances():
         p, ng, s = tile_config("float", 32, 32, True, cf)
         in_mode, out_mode = (0, 1) if cf else (1, 0)
         out.append(("float", 32, 32, p, rc, cc, cf, in_mode, out_mode, ng, s))
+    # mixed-shape gather kernels (config 3): fp32, the four C3 shapes, pre + post
+    for h, w in ((16, 16), (16, 32), (32, 16), (32, 32)):
+        for rc, cc, cf in two_d_pairs():
+            if rc in (code(DCT2), code(IDCT2)) or (rc >> 8) == 4:
+                continue
+            p, ng, s = tile_config("float", h, w, True, cf)
+            out.append(("float", h, w, min(p, 32), rc, cc, cf, 2, 2, ng, s))
     # identity-op tile round trip (TMA in -> smem -> TMA out, no arithmetic):
     # the data-movement ceiling of the tile pipeline (dctadj_copy_tiles)
     for dt in DTYPES:

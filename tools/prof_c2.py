@@ -16,13 +16,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--iters", type=int, default=3)
 a = ap.parse_args()
-cfg = bench.CONFIGS[a.config]
-th, tv = cfg["transforms"]()
-x = getattr(workloads, cfg["inputs"])("cuda", cfg["blocks"])
+wl, nblk, n, dt, make, inputs, inverse = bench.UNIFORM[a.config]
+th = tv = make()
+x = getattr(workloads, inputs)("cuda", nblk)
 torch.cuda.synchronize()
 for _ in range(a.iters):
     y = pipeline.forward_adjusted_2d(th, tv, x)
-    if cfg["inverse"]:
+    if inverse:
         pipeline.inverse_adjusted_2d(th, tv, y)
 torch.cuda.synchronize()
 print("ok")
