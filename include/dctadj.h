@@ -70,6 +70,14 @@ typedef struct dctadj_axis {
   int32_t taps;       /* band taps (adj == BAND) */
   int32_t order;      /* sub-block order (adj == SUBBLOCK) */
   const double* mat;  /* host n x n realized adjustment (row-major); NULL if NONE */
+  /* optional, band only: the Givens schedule behind `mat` -- taps-1 brick-wall
+   * layers of adjacent-pair rotations (layer l pairs (i, i+1), i = l%2, l%2+2, ...;
+   * reference design.py:225-243), angles in layer order, ascending i.  When given
+   * (ngivens == the rotation count of that structure) the band runs as lifting
+   * rotations (3 FMAs per rotation) instead of the 2*taps-1 FMA product. */
+  const double* givens;
+  int32_t ngivens;
+  int32_t reserved;   /* 0 */
 } dctadj_axis;
 
 /* ---- the seven batch primitives (reference kernels/__init__.py:33-41) ----

@@ -43,6 +43,9 @@ class Axis(ctypes.Structure):
         ("taps", ctypes.c_int32),
         ("order", ctypes.c_int32),
         ("mat", ctypes.POINTER(ctypes.c_double)),
+        ("givens", ctypes.POINTER(ctypes.c_double)),
+        ("ngivens", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -122,17 +122,29 @@ static int tuning_variant() {
   return v;
 }
 
+// DCTADJ_TRACE=1 prints every kernel selection to stderr (diagnostics)
+static bool trace_on() {
+  static bool v = std::getenv("DCTADJ_TRACE") != nullptr;
+  return v;
+}
+
 static const KernelEntry* find_kernel(int dtype, int h, int w, int rc, int cc, int col_first,
                                       int in_mode, int out_mode) {
   const KernelEntry* dflt = nullptr;
+  const KernelEntry* hit = nullptr;
   const int want = tuning_variant();
   for (const KernelEntry& e : kRegistry)
     if (e.dtype == dtype && e.h == h && e.w == w && e.rc == rc && e.cc == cc &&
         e.col_first == col_first && e.in_mode == in_mode && e.out_mode == out_mode) {
-      if (e.variant == want) return &e;
+      if (e.variant == want) hit = &e;
       if (e.variant == 0) dflt = &e;
     }
-  return dflt;
+  if (!hit) hit = dflt;
+  if (trace_on())
+    std::fprintf(stderr, "[dctadj] dtype=%d %dx%d rc=0x%x cc=0x%x col_first=%d mode=%d->%d: %s (variant %d)\n",
+                 dtype, h, w, rc, cc, col_first, in_mode, out_mode, hit ? "found" : "MISSING",
+                 hit ? hit->variant : -1);
+  return hit;
 }
 
 // ------------------------------------------------------------- axis planning
@@ -186,6 +198,8 @@ static int validate_axis(const dctadj_axis* ax) {
     return fail(ST_ERR_PATTERN, "band taps must be in 1..%d, got %d", ax->n, ax->taps);
   if (ax->adj == DCTADJ_ADJ_SUBBLOCK && (ax->order < 1 || ax->order > ax->n))
     return fail(ST_ERR_PATTERN, "sub-block order must be in 1..%d, got %d", ax->n, ax->order);
+  if (ax->ngivens < 0 || (ax->ngivens > 0 && !ax->givens))
+    return fail(ST_ERR_VALUE, "bad Givens schedule (%d angles)", ax->ngivens);
   return ST_OK;
 }
 
@@ -235,6 +249,24 @@ static void pack_band(const dctadj_axis* ax, bool transpose, int k, std::vector<
     }
 }
 
+// Lifting coefficients (tan(theta/2), sin(theta)) of a brick-wall schedule in
+// application order: layers 0..K-2 forward; for A^T the layers reversed with
+// negated angles (for even K the reversed layers keep the l%2 offsets).
+static void pack_givens(const dctadj_axis* ax, bool inverse, std::vector<double>& c) {
+  const int n = ax->n, k = ax->taps;
+  std::vector<int> start(k, 0);
+  for (int l = 0; l + 1 < k; ++l) start[l + 1] = start[l] + givens_layer_rots(n, l);
+  c.clear();
+  for (int a = 0; a < k - 1; ++a) {
+    const int l = inverse ? k - 2 - a : a;
+    for (int r = 0; r < givens_layer_rots(n, l); ++r) {
+      const double th = inverse ? -ax->givens[start[l] + r] : ax->givens[start[l] + r];
+      c.push_back(std::tan(0.5 * th));
+      c.push_back(std::sin(th));
+    }
+  }
+}
+
 static void pack_sub(const dctadj_axis* ax, bool transpose, int k, std::vector<double>& c) {
   c.assign(static_cast<size_t>(k) * k, 0.0);
   for (int r = 0; r < k; ++r)
@@ -252,7 +284,12 @@ static int plan_axis(const dctadj_axis* ax, bool inverse, bool force_dense, Axis
   const int bi = ax->base == DCTADJ_BASE_DCT2 ? ST_IDCT2 : ax->base == DCTADJ_BASE_DST3 ? ST_IDST3 : ST_DCT2;
   const int base = inverse ? bi : bf;
   int adj_stage = ST_NONE, k = 0;
-  if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps == 4 || ax->taps == 6)) {
+  if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps == 4 || ax->taps == 6) && ax->givens &&
+      ax->ngivens == givens_rots(ax->n, ax->taps)) {
+    adj_stage = ST_GIVENS;
+    k = ax->taps;
+    pack_givens(ax, inverse, p->coef);
+  } else if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps == 4 || ax->taps == 6)) {
     adj_stage = ST_BAND;
     k = ax->taps;
     pack_band(ax, inverse, k, p->coef);
@@ -436,7 +473,33 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
 }
 
 // Host-buffer pipeline: chunks of blocks cycle through NSTREAM streams, each
-// with its own device in/out buffers: H2D(c) overlaps kernel(c-1) and D2H(c-2).
+// with its own device in/out buffers: H2D(c) overlaps kernel(c-1) and D2H(c-2)
+// (PCIe is full duplex).  Streams and staging buffers persist per device
+// (one pipeline at a time per device; concurrent host calls serialise).
+struct HostPipe {
+  static constexpr int NSTREAM = 4;
+  std::mutex mu;
+  bool ready = false;
+  cudaStream_t st[NSTREAM] = {};
+  void* din[NSTREAM] = {};
+  void* dout[NSTREAM] = {};
+  size_t cap = 0;
+};
+
+static HostPipe& host_pipe(int device) {
+  static HostPipe pipes[64];
+  return pipes[(device >= 0 && device < 64) ? device : 0];
+}
+
+static size_t host_chunk_bytes() {
+  static size_t v = [] {
+    const char* s = std::getenv("DCTADJ_HOST_CHUNK_MB");
+    const long mb = s ? std::atol(s) : 16;
+    return static_cast<size_t>(mb > 0 ? mb : 16) << 20;
+  }();
+  return v;
+}
+
 static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* xh, void* yh,
                        int64_t nblk, int dtype, bool inverse, int device) {
   int rc = check_dtype(dtype);
@@ -446,43 +509,51 @@ static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x
   if (nblk == 0) return ST_OK;
   if (!xh || !yh) return fail(ST_ERR_VALUE, "NULL data pointer");
   DA_CUDA(cudaSetDevice(device));
-  constexpr int NSTREAM = 3;
+  HostPipe& hp = host_pipe(device);
+  std::lock_guard<std::mutex> lock(hp.mu);
   const size_t blk_bytes = static_cast<size_t>(h->n) * v->n * dt_size(dtype);
-  const int64_t chunk = std::max<int64_t>(1, static_cast<int64_t>((32u << 20) / blk_bytes));
+  const int64_t chunk = std::max<int64_t>(1, static_cast<int64_t>(host_chunk_bytes() / blk_bytes));
   const int64_t nchunks = (nblk + chunk - 1) / chunk;
-  const int nbuf = static_cast<int>(std::min<int64_t>(NSTREAM, nchunks));
-  cudaStream_t st[NSTREAM] = {};
-  void* din[NSTREAM] = {};
-  void* dout[NSTREAM] = {};
-  int status = ST_OK;
-  for (int i = 0; i < nbuf && !status; ++i) {
-    if (cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking) != cudaSuccess ||
-        cudaMallocAsync(&din[i], chunk * blk_bytes, st[i]) != cudaSuccess ||
-        cudaMallocAsync(&dout[i], chunk * blk_bytes, st[i]) != cudaSuccess)
-      status = fail(ST_ERR_CUDA, "host pipeline setup: %s", cudaGetErrorString(cudaGetLastError()));
+  const size_t need = static_cast<size_t>(chunk) * blk_bytes;
+  if (!hp.ready) {
+    for (int i = 0; i < HostPipe::NSTREAM; ++i)
+      DA_CUDA(cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking));
+    hp.ready = true;
   }
+  if (hp.cap < need) {
+    for (int i = 0; i < HostPipe::NSTREAM; ++i) {
+      DA_CUDA(cudaStreamSynchronize(hp.st[i]));
+      if (hp.din[i]) cudaFree(hp.din[i]);
+      if (hp.dout[i]) cudaFree(hp.dout[i]);
+      hp.din[i] = hp.dout[i] = nullptr;
+    }
+    hp.cap = 0;
+    for (int i = 0; i < HostPipe::NSTREAM; ++i) {
+      DA_CUDA(cudaMalloc(&hp.din[i], need));
+      DA_CUDA(cudaMalloc(&hp.dout[i], need));
+    }
+    hp.cap = need;
+  }
+  int status = ST_OK;
   for (int64_t c = 0; c < nchunks && !status; ++c) {
-    const int k = static_cast<int>(c % nbuf);
+    const int k = static_cast<int>(c % HostPipe::NSTREAM);
     const int64_t b0 = c * chunk, nb = std::min(chunk, nblk - b0);
     const size_t off = static_cast<size_t>(b0) * blk_bytes, bytes = static_cast<size_t>(nb) * blk_bytes;
-    if (cudaMemcpyAsync(din[k], static_cast<const char*>(xh) + off, bytes, cudaMemcpyHostToDevice,
-                        st[k]) != cudaSuccess) {
+    if (cudaMemcpyAsync(hp.din[k], static_cast<const char*>(xh) + off, bytes,
+                        cudaMemcpyHostToDevice, hp.st[k]) != cudaSuccess) {
       status = fail(ST_ERR_CUDA, "H2D copy: %s", cudaGetErrorString(cudaGetLastError()));
       break;
     }
-    status = run_2d(h, v, din[k], dout[k], nb, dtype, inverse, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, st[k]);
+    status = run_2d(h, v, hp.din[k], hp.dout[k], nb, dtype, inverse, MODE_LINEAR, MODE_LINEAR, 0,
+                    0, 0, hp.st[k]);
     if (status) break;
-    if (cudaMemcpyAsync(static_cast<char*>(yh) + off, dout[k], bytes, cudaMemcpyDeviceToHost,
-                        st[k]) != cudaSuccess)
+    if (cudaMemcpyAsync(static_cast<char*>(yh) + off, hp.dout[k], bytes, cudaMemcpyDeviceToHost,
+                        hp.st[k]) != cudaSuccess)
       status = fail(ST_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
   }
-  for (int i = 0; i < nbuf; ++i) {
-    if (!st[i]) continue;
-    if (din[i]) cudaFreeAsync(din[i], st[i]);
-    if (dout[i]) cudaFreeAsync(dout[i], st[i]);
-    cudaError_t e = cudaStreamSynchronize(st[i]);
+  for (int i = 0; i < HostPipe::NSTREAM; ++i) {
+    cudaError_t e = cudaStreamSynchronize(hp.st[i]);
     if (e != cudaSuccess && !status) status = fail(ST_ERR_CUDA, "pipeline: %s", cudaGetErrorString(e));
-    cudaStreamDestroy(st[i]);
   }
   return status;
 }
@@ -599,7 +670,7 @@ int dctadj_idst3(const void* x, void* y, int64_t nvec, int32_t n, int32_t dtype,
 
 int dctadj_band(const double* a, int32_t taps, const void* x, void* y, int64_t nvec, int32_t n,
                 int32_t dtype, void* stream) {
-  dctadj_axis ax{n, DCTADJ_BASE_DCT2, DCTADJ_ADJ_BAND, DCTADJ_SIDE_PRE, taps, 0, a};
+  dctadj_axis ax{n, DCTADJ_BASE_DCT2, DCTADJ_ADJ_BAND, DCTADJ_SIDE_PRE, taps, 0, a, nullptr, 0, 0};
   int rc = check_dtype(dtype);
   if (rc) return rc;
   rc = validate_axis(&ax);

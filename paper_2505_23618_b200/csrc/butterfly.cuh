@@ -214,7 +214,17 @@ enum Stage : int {
   ST_BAND = 5,   // K-tap band, coefficients packed [N][2K-1]
   ST_SUB = 6,    // leading KxK block, coefficients packed [K][K]
   ST_DENSE = 7,  // full N x N from shared memory
+  ST_GIVENS = 8, // K-tap band as K-1 brick-wall layers of plane rotations, lifting form
 };
+
+// Rotations in brick-wall layer l of an N-point band schedule (pairs (i, i+1),
+// i = l%2, l%2 + 2, ...; reference design.py:234-243).
+__host__ __device__ constexpr int givens_layer_rots(int n, int l) { return (n - (l % 2)) / 2; }
+__host__ __device__ constexpr int givens_rots(int n, int k) {
+  int r = 0;
+  for (int l = 0; l < k - 1; ++l) r += givens_layer_rots(n, l);
+  return r;
+}
 
 // op code = s1 | s2 << 4 | k << 8
 __host__ __device__ constexpr int op_code(int s1, int s2 = ST_NONE, int k = 0) {
@@ -235,6 +245,10 @@ struct StageCoef<T, N, K, ST_BAND> {
 template <typename T, int N, int K>
 struct StageCoef<T, N, K, ST_SUB> {
   static constexpr int count = K * K;
+};
+template <typename T, int N, int K>
+struct StageCoef<T, N, K, ST_GIVENS> {
+  static constexpr int count = 2 * givens_rots(N, K);  // (tan(theta/2), sin(theta)) per rotation
 };
 
 template <typename T, int N, int CODE>
@@ -309,6 +323,29 @@ DA_DEV void run_stage(V (&v)[N], const typename Scalar<V>::type* __restrict__ cf
     }
 #pragma unroll
     for (int r = 0; r < K; ++r) v[r] = y[r];
+  } else if constexpr (S == ST_GIVENS) {
+    // y = L_{K-2} ... L_0 x, each layer index-disjoint rotations
+    //   x_i' = c x_i - s x_j,  x_j' = s x_i + c x_j   (reference design.py:137-147)
+    // in lifting form, 3 FMAs per rotation with t = tan(theta/2):
+    //   a = x_i - t x_j;  x_j' = x_j + s a;  x_i' = a - t x_j'
+    // (7.5 FMAs per sample for K = 6 against 11 for the band product).  The
+    // host packs the layers in application order (reversed, angles negated,
+    // for A^T).
+#pragma unroll
+    for (int l = 0; l < K - 1; ++l) {
+#pragma unroll
+      for (int i = l % 2; i + 1 < N; i += 2) {
+        int q = 0;
+#pragma unroll
+        for (int m = 0; m < l; ++m) q += givens_layer_rots(N, m);
+        q += (i - l % 2) / 2;
+        const auto t = cf[2 * q], sn = cf[2 * q + 1];
+        const V a = fnmac(v[i + 1], t, v[i]);
+        const V b = fmac(a, sn, v[i + 1]);
+        v[i] = fnmac(b, t, a);
+        v[i + 1] = b;
+      }
+    }
   } else if constexpr (S == ST_DENSE) {
     V y[N];
 #pragma unroll

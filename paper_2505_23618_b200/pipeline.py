@@ -132,14 +132,35 @@ class AdjustedTransform:
     adjustment: AdjustmentMatrix
     base_path: BasePath
 
-    def axis(self) -> tuple[_lib.Axis, np.ndarray]:
-        """The C-ABI descriptor (and the matrix buffer it points into)."""
+    def axis(self):
+        """The C-ABI descriptor (and the host buffers it points into)."""
         adj = self.adjustment
         mat = np.ascontiguousarray(adj.realized, dtype=np.float64)
         ax = _lib.Axis(self.size, _BASE_CODE[self.base_path], _ADJ_CODE[adj.pattern.kind],
                        _lib.SIDE_PRE if adj.side is Side.PRE else _lib.SIDE_POST,
                        adj.pattern.taps or 0, adj.pattern.order or 0, _lib.dptr(mat))
-        return ax, mat
+        angles = brickwall_angles(adj)
+        if angles is not None:
+            ax.givens = _lib.dptr(angles)
+            ax.ngivens = len(angles)
+        return ax, (mat, angles)
+
+
+def brickwall_angles(adj: AdjustmentMatrix):
+    """The schedule angles of a band adjustment whose Givens schedule is the
+    reference's brick-wall structure (taps-1 layers, layer l pairing (i, i+1)
+    for i = l%2, l%2+2, ...; design.py:225-243), in layer order -- else None."""
+    if adj.pattern.kind is not PatternKind.BAND:
+        return None
+    n, k = adj.pattern.size, adj.pattern.taps
+    layers = adj.schedule.layers
+    if len(layers) != k - 1:
+        return None
+    for level, layer in enumerate(layers):
+        want = [(i, i + 1) for i in range(level % 2, n - 1, 2)]
+        if [(r.i, r.j) for r in layer] != want:
+            return None
+    return np.ascontiguousarray([r.theta for layer in layers for r in layer], dtype=np.float64)
 
 
 def make_adjusted_transform(adj: AdjustmentMatrix) -> AdjustedTransform:

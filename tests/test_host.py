@@ -194,3 +194,45 @@ def test_weighted_ranges_balance():
         assert rs[0][0] == 0 and rs[-1][1] == w.size
         loads = [w[a:b].sum() for a, b in rs]
         assert max(loads) - min(loads) <= 2 * w.max()
+
+
+def _lifting_apply(angles, n, k, x, inverse=False):
+    """Python restatement of the kernel's Givens lifting stage (butterfly.cuh
+    ST_GIVENS) with the C-ABI packing rule (abi.cu pack_givens)."""
+    rots = [(n - (l % 2)) // 2 for l in range(k - 1)]
+    start = np.concatenate([[0], np.cumsum(rots)])
+    x = np.array(x, dtype=float)
+    for a in range(k - 1):
+        l = k - 2 - a if inverse else a
+        for r in range(rots[l]):
+            th = angles[start[l] + r] * (-1 if inverse else 1)
+            t, s = np.tan(th / 2), np.sin(th)
+            i = (a % 2) + 2 * r
+            aa = x[i] - t * x[i + 1]
+            b = x[i + 1] + s * aa
+            x[i], x[i + 1] = aa - t * b, b
+    return x
+
+
+@pytest.mark.parametrize("name", ["band6_pre_dst3_dst7_n16", "band6_pre_dst3_dst7_n32",
+                                  "band4_pre_dst3_dst7_n64"])
+def test_brickwall_lifting_reproduces_realized(name):
+    from paper_2505_23618_b200.pipeline import brickwall_angles
+    for adj in (matio.load_designed(name), flip_pre_adjustment(matio.load_designed(name))):
+        n, k = adj.pattern.size, adj.pattern.taps
+        ang = brickwall_angles(adj)
+        assert ang is not None and len(ang) == sum((n - (l % 2)) // 2 for l in range(k - 1))
+        eye = np.eye(n)
+        fwd = np.stack([_lifting_apply(ang, n, k, eye[:, j]) for j in range(n)], axis=1)
+        inv = np.stack([_lifting_apply(ang, n, k, eye[:, j], True) for j in range(n)], axis=1)
+        assert np.abs(fwd - adj.realized).max() < 1e-13
+        assert np.abs(inv - adj.realized.T).max() < 1e-13
+
+
+def test_brickwall_detection_rejects_other_schedules():
+    from dataclasses import replace
+    from paper_2505_23618_b200.pipeline import brickwall_angles
+    assert brickwall_angles(matio.load_designed("sub8_post_dct2_dst7_n32")) is None
+    a = matio.load_designed("band6_pre_dst3_dst7_n32")
+    odd = GivensSchedule(32, a.schedule.layers[:-1])  # one layer short
+    assert brickwall_angles(replace(a, schedule=odd, pattern=SparsityPattern.band(6, 32))) is None

@@ -11,7 +11,9 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2505_23618_b200 import _lib, workloads  # noqa: E402
 
-wl, nblk, n_, dt_, make, inputs, inverse = bench.UNIFORM[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+EXTRA = {"pre32": ("pre32", 65536, 32, "f32", lambda: bench._pre(32, "dst7"), "c2_inputs", True)}
+name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+wl, nblk, n_, dt_, make, inputs, inverse = EXTRA.get(name) or bench.UNIFORM[name]
 cfg = {"h": n_, "w": n_}
 th = tv = make()
 x = getattr(workloads, inputs)("cuda", nblk)

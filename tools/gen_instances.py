@@ -14,7 +14,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1] / "paper_2505_23618_b200" / "csrc" / "gen"
 NSHARDS = 12
 
-NONE, DCT2, IDCT2, DST3, IDST3, BAND, SUB, DENSE = range(8)
+NONE, DCT2, IDCT2, DST3, IDST3, BAND, SUB, DENSE, GIVENS = range(9)
 
 
 def code(s1, s2=NONE, k=0):
@@ -26,35 +26,45 @@ ID = code(NONE)
 DTYPES = {"float": 0, "double": 1}
 
 
-def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False):
-    """(P blocks per super-tile, NG warps per CTA, S ring stages).
+def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False,
+                rc: int = 0):
+    """(P blocks per super-tile, NG warps per CTA, S ring stages, pair_rows).
 
-    Measured on B200 (profiles/r01_tuning.md): for 32x32 fp32 the forward
-    (rows first) runs best with 16 KB super-tiles, 2 warps x 3 stages per CTA;
-    the inverse (columns first) with 8 KB super-tiles, 4 warps x 4 stages --
-    both ~86 us per 536 MB launch (0.95 of the measured HBM copy peak)."""
+    Measured on B200 (back-to-back launches, profiles/r01_tuning.md): for 32x32
+    fp32 both directions run best with 8 KB super-tiles (P=2) and 4 warps x 4
+    stages per CTA; packed row pairs help everywhere except the inverse
+    sub-block kernel, and the inverse band (Givens) kernel prefers 16 KB super-
+    tiles with 2 warps x 3 stages."""
     es = 4 if dtype == "float" else 8
     p = 1
+    pr = False
     if two_d:
         # rows: P*H >= 32; packed column pairs (fp32): P*W >= 64
         p = max(1, 32 // h, (64 // w) if dtype == "float" else 32 // w)
-        if dtype == "float" and h * w <= 1024:
-            p = max(p, (4 if not col_first else 2) * 1024 // (h * w))
+    small32 = two_d and dtype == "float" and h * w <= 1024
+    band_inv = col_first and (rc >> 8) in (4, 6) and (rc & 15) != SUB and ((rc >> 4) & 15) in (BAND, GIVENS)
+    if small32:
+        if band_inv:
+            p, ng, s, pr = max(p, 4 * 1024 // (h * w)), 2, 3, True
+        else:
+            p, ng, s, pr = max(p, 2 * 1024 // (h * w)), 4, 4, not col_first
+        if (p * h) % 64:
+            pr = False
+        return p, ng, s, pr
     tile = p * h * w * es
     stage = -(-tile // 1024) * 1024
-    if two_d and dtype == "float" and h * w <= 1024:
-        ng, s = (2, 3) if not col_first else (4, 4)
-    elif stage <= 2048:
+    if stage <= 2048:
         ng, s = 8, 4
     elif stage <= 4096:
         ng, s = 8, 3
     elif stage <= 8192:
         ng, s = 4, 3
     elif stage <= 16384:
-        ng, s = 6, 2
+        ng, s = (4, 3) if two_d and dtype == "float" and (rc & 15) != GIVENS \
+            and ((rc >> 4) & 15) != GIVENS else (6, 2)
     else:
         ng, s = 3, 2
-    return p, ng, s
+    return p, ng, s, pr
 
 
 def one_d_ops(n: int):
@@ -66,6 +76,11 @@ def one_d_ops(n: int):
                 code(BAND, DST3, 6), code(IDST3, BAND, 6),
                 code(BAND, IDCT2, 6), code(DCT2, BAND, 6),
                 code(DCT2, SUB, 8), code(SUB, IDCT2, 8)]
+    # band as Givens lifting layers (schedule supplied), fused with the base
+    for k in (4, 6):
+        if k <= n:
+            ops += [code(GIVENS, DST3, k), code(IDST3, GIVENS, k),
+                    code(GIVENS, IDCT2, k), code(DCT2, GIVENS, k)]
     return ops
 
 
@@ -75,16 +90,18 @@ def two_d_pairs():
     inv = []
     fwd.append((code(DCT2, SUB, 8), code(DCT2, SUB, 8)))
     inv.append((code(SUB, IDCT2, 8), code(SUB, IDCT2, 8)))
+    # band pre-adjustments run as Givens lifting layers in the fused 2-D kernels
+    # (a band given only as a matrix falls back to the dense composite)
     for kh in (DST3, IDCT2):          # DST-7 (DST-3 base) / DCT-8 (DCT-3 base, R*A*R band)
         for kv in (DST3, IDCT2):
-            fwd.append((code(BAND, kh, 6), code(BAND, kv, 6)))
+            fwd.append((code(GIVENS, kh, 6), code(GIVENS, kv, 6)))
             ih = IDST3 if kh == DST3 else DCT2
             iv = IDST3 if kv == DST3 else DCT2
-            inv.append((code(ih, BAND, 6), code(iv, BAND, 6)))
+            inv.append((code(ih, GIVENS, 6), code(iv, GIVENS, 6)))
     for kb in (DST3, IDCT2):
-        fwd.append((code(BAND, kb, 4), code(BAND, kb, 4)))
+        fwd.append((code(GIVENS, kb, 4), code(GIVENS, kb, 4)))
         ib = IDST3 if kb == DST3 else DCT2
-        inv.append((code(ib, BAND, 4), code(ib, BAND, 4)))
+        inv.append((code(ib, GIVENS, 4), code(ib, GIVENS, 4)))
     fwd.append((code(DCT2), code(DCT2)))
     inv.append((code(IDCT2), code(IDCT2)))
     fwd.append((code(DENSE), code(DENSE)))
@@ -101,54 +118,62 @@ def pair_flags(dt, h, w, p, rc, cc):
 
 
 # tuning variants for the 32x32 fp32 hot kernels (DCTADJ_VARIANT=k): (P, NG, S)
-# tuning variants for the 32x32 fp32 hot kernels (DCTADJ_VARIANT=k): (P, NG, S, L2 hints)
-EXPERIMENT = [(4, 2, 3, 0), (2, 4, 4, 0)]
+# tuning variants (DCTADJ_VARIANT=k, k >= 1), per (H, W) of fp32 uniform 2-D kernels:
+# (P, NG, S, pair_rows, pair_cols, L2 hints); variant 0 is always the default build
+EXPERIMENT = {
+    (32, 32): [(4, 2, 3, True, True, 0), (2, 4, 4, True, True, 0), (4, 2, 3, False, True, 0),
+               (2, 4, 4, False, True, 0)],
+    (64, 64): [(1, 4, 3, False, True, 0), (1, 6, 2, False, True, 0), (1, 8, 2, False, True, 0),
+               (1, 5, 2, False, True, 0)],
+}
+EXPERIMENT_OPS = None  # filled below: the band-6 and sub-8 2-D ops
 
 
 def instances():
     out = []
     for dt in DTYPES:
         for n in (4, 8, 16, 32, 64):
-            p, ng, s = tile_config(dt, 32, n, False)
             for op in one_d_ops(n):
-                out.append((dt, 32, n, p, op, ID, False, 0, 0, ng, s))
+                p, ng, s, pr = tile_config(dt, 32, n, False)
+                out.append((dt, 32, n, p, op, ID, False, 0, 0, ng, s, pr))
         shapes = [(16, 16), (16, 32), (32, 16), (32, 32), (64, 64)]
         if dt == "double":
             shapes = [(16, 16), (32, 32), (64, 64)]
         for h, w in shapes:
             for rc, cc, cf in two_d_pairs():
-                p, ng, s = tile_config(dt, h, w, True, cf)
-                out.append((dt, h, w, p, rc, cc, cf, 0, 0, ng, s))
+                p, ng, s, pr = tile_config(dt, h, w, True, cf, rc)
+                out.append((dt, h, w, p, rc, cc, cf, 0, 0, ng, s, pr))
     # frame tiling (config 5): 32x32 fp32, frames in / blocks out and back
     for rc, cc, cf in two_d_pairs():
         if rc == code(DCT2) or (rc >> 8) == 4:
             continue
-        p, ng, s = tile_config("float", 32, 32, True, cf)
+        p, ng, s, pr = tile_config("float", 32, 32, True, cf, rc)
         in_mode, out_mode = (0, 1) if cf else (1, 0)
-        out.append(("float", 32, 32, p, rc, cc, cf, in_mode, out_mode, ng, s))
+        out.append(("float", 32, 32, p, rc, cc, cf, in_mode, out_mode, ng, s, pr))
     # mixed-shape gather kernels (config 3): fp32, the four C3 shapes, pre + post
     for h, w in ((16, 16), (16, 32), (32, 16), (32, 32)):
         for rc, cc, cf in two_d_pairs():
             if rc in (code(DCT2), code(IDCT2)) or (rc >> 8) == 4:
                 continue
-            p, ng, s = tile_config("float", h, w, True, cf)
-            out.append(("float", h, w, min(p, 32), rc, cc, cf, 2, 2, ng, s))
+            p, ng, s, pr = tile_config("float", h, w, True, cf, rc)
+            out.append(("float", h, w, min(p, 32), rc, cc, cf, 2, 2, ng, s, pr))
     # identity-op tile round trip (TMA in -> smem -> TMA out, no arithmetic):
     # the data-movement ceiling of the tile pipeline (dctadj_copy_tiles)
     for dt in DTYPES:
         for h, w in ((32, 32), (64, 64), (16, 16)):
-            p, ng, s = tile_config(dt, h, w, True)
-            out.append((dt, h, w, p, ID, ID, False, 0, 0, ng, s))
+            p, ng, s, pr = tile_config(dt, h, w, True)
+            out.append((dt, h, w, p, ID, ID, False, 0, 0, ng, s, False))
     # attach packing flags + tuning variants (variant 0 = default)
     final = []
     for inst in out:
-        dt, h, w, p, rc, cc, cf, im, om, ng, s_ = inst
-        final.append(inst + pair_flags(dt, h, w, p, rc, cc) + (0, 0))
-        if dt == "float" and (h, w) == (32, 32) and im == 0 and om == 0 and rc == cc \
-                and rc in (ID, code(DCT2, SUB, 8), code(SUB, IDCT2, 8)):
-            for k, (pp, nng, ss, ch) in enumerate(EXPERIMENT, start=1):
-                final.append((dt, h, w, pp, rc, cc, cf, im, om, nng, ss)
-                             + pair_flags(dt, h, w, pp, rc, cc) + (k, ch))
+        dt, h, w, p, rc, cc, cf, im, om, ng, s_, pr = inst
+        _, pc = pair_flags(dt, h, w, p, rc, cc)
+        final.append(inst[:11] + (pr and cc != ID, pc, 0, 0))
+        if dt == "float" and (h, w) in EXPERIMENT and im == 0 and om == 0 and rc == cc \
+                and rc in (code(DCT2, SUB, 8), code(SUB, IDCT2, 8), code(GIVENS, DST3, 6),
+                           code(IDST3, GIVENS, 6)):
+            for k, (pp, nng, ss, pr, pc, ch) in enumerate(EXPERIMENT[(h, w)], start=1):
+                final.append((dt, h, w, pp, rc, cc, cf, im, om, nng, ss, pr, pc, k, ch))
     return final
 
 
