@@ -128,6 +128,16 @@ int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void
                           void* frames, int32_t nframes, int32_t height, int32_t width,
                           int32_t dtype, void* stream);
 
+/* ---- simultaneous encoder evaluation (reference pipeline.py:256-293, paper
+ * Table 1 "Multiple"): for each (H, W) block, one read, one shared 2-D DCT-2 and
+ * five coefficient planes, planes[k] (device, each (nblk, H, W)):
+ *   0 (dct2, dct2)  1 (dst7, dst7)  2 (dct8, dst7)  3 (dst7, dct8)  4 (dct8, dct8)
+ * keyed (horizontal, vertical).  h / v: post sub-block DCT-2 -> DST-7 axes (the
+ * DCT-8 planes use C8 = S C7 S, design.py:677-715).  Coefficients outside the
+ * leading 8 rows / columns are bit-identical across all five planes. */
+int dctadj_encoder_eval(const dctadj_axis* h, const dctadj_axis* v, const void* x,
+                        void* const* planes, int64_t nblk, int32_t dtype, void* stream);
+
 /* ---- mixed-shape batches (config 3): blocks of different sizes packed back
  * to back in one buffer of `total_elements` samples.  Block i starts at element
  * offsets[i] (a multiple of its width), its rows use axis-table entry

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/dctadj.h"
+#include "enc5.cuh"
 #include "launch.cuh"
 
 namespace dctadj {
@@ -573,6 +574,120 @@ static int run_frames(const dctadj_axis* h, const dctadj_axis* v, const void* in
                 inverse ? MODE_FRAME : MODE_LINEAR, nframes, height, width, st);
 }
 
+// ------------------------------------------------------------- encoder evaluation
+template <typename T, int H, int W, int P, int NG, int S>
+static int launch_enc5(const void* x, void* const* outs, int64_t nblk, const double* cv,
+                       const double* ch, cudaStream_t st) {
+  using L = TileLayout<T, H, W, P>;
+  Geom g{};
+  g.ntiles = (nblk * H + L::PH - 1) / L::PH;
+  g.nblocks = g.ntiles * P;
+  LaunchArgs a;
+  a.rows = nblk * H;
+  CUtensorMap in_map, om[5];
+  int rc = make_map<T, H, W, P, MODE_LINEAR>(&in_map, x, a);
+  for (int i = 0; i < 5 && !rc; ++i) rc = make_map<T, H, W, P, MODE_LINEAR>(&om[i], outs[i], a);
+  if (rc) return rc;
+  Enc5Params<T> prm;
+  for (int i = 0; i < 64; ++i) {
+    prm.cv[i] = static_cast<T>(cv[i]);
+    prm.ch[i] = static_cast<T>(ch[i]);
+  }
+  auto kern = enc5_kernel<T, H, W, P, NG, S>;
+  const size_t smem = 1024 + static_cast<size_t>(NG) * (S + 4) * L::STAGEB + NG * S * 8;
+  static int bps = 0;
+  if (!bps) {
+    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NG * 32, smem));
+    if (bps < 1) return fail(ST_ERR_CUDA, "enc5 kernel does not fit an SM");
+  }
+  const int64_t want = (g.ntiles + NG - 1) / NG;
+  const int64_t cap = static_cast<int64_t>(num_sms_cached()) * bps;
+  kern<<<static_cast<int>(std::min(want, cap)), NG * 32, smem, st>>>(in_map, om[0], om[1], om[2],
+                                                                    om[3], om[4], g, prm);
+  DA_CUDA(cudaGetLastError());
+  return ST_OK;
+}
+
+using Enc5Fn = int (*)(const void*, void* const*, int64_t, const double*, const double*,
+                       cudaStream_t);
+struct Enc5Entry {
+  int dtype, h, w;
+  Enc5Fn fn;
+};
+static const Enc5Entry kEnc5[] = {
+    {0, 16, 16, &launch_enc5<float, 16, 16, 2, 4, 2>},
+    {0, 16, 32, &launch_enc5<float, 16, 32, 2, 4, 2>},
+    {0, 32, 16, &launch_enc5<float, 32, 16, 2, 4, 2>},
+    {0, 32, 32, &launch_enc5<float, 32, 32, 1, 4, 2>},
+    {0, 32, 64, &launch_enc5<float, 32, 64, 1, 2, 2>},
+    {0, 64, 32, &launch_enc5<float, 64, 32, 1, 2, 2>},
+    {0, 64, 64, &launch_enc5<float, 64, 64, 1, 1, 2>},
+    {1, 16, 16, &launch_enc5<double, 16, 16, 2, 2, 2>},
+    {1, 32, 32, &launch_enc5<double, 32, 32, 1, 2, 2>},
+    {1, 32, 64, &launch_enc5<double, 32, 64, 1, 1, 2>},
+    {1, 64, 32, &launch_enc5<double, 64, 32, 1, 1, 2>},
+    {1, 64, 64, &launch_enc5<double, 64, 64, 1, 1, 2>},
+};
+
+static int check_enc_axis(const dctadj_axis* a, const char* name) {
+  int rc = validate_axis(a);
+  if (rc) return rc;
+  if (a->adj != DCTADJ_ADJ_SUBBLOCK)
+    return fail(ST_ERR_CONFIG, "%s adjustment must be a sub-block design", name);
+  if (a->side != DCTADJ_SIDE_POST || a->base != DCTADJ_BASE_DCT2)
+    return fail(ST_ERR_CONFIG, "%s adjustment must be post-side dct2 -> dst7", name);
+  return ST_OK;
+}
+
+// C8 = S C7 S of a post sub-block axis (reference design.py:677-715)
+static void chessboard(const dctadj_axis* a, std::vector<double>& m8) {
+  const int n = a->n;
+  m8.assign(a->mat, a->mat + static_cast<size_t>(n) * n);
+  for (int r = 0; r < n; ++r)
+    for (int j = 0; j < n; ++j)
+      if ((r + j) & 1) m8[r * n + j] = -m8[r * n + j];
+}
+
+static int run_enc5(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* const* outs,
+                    int64_t nblk, int dtype, cudaStream_t st) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if ((rc = check_enc_axis(h, "horizontal")) || (rc = check_enc_axis(v, "vertical"))) return rc;
+  if (nblk < 0) return fail(ST_ERR_SHAPE, "negative block count");
+  if (nblk == 0) return ST_OK;
+  if (!x || !outs) return fail(ST_ERR_VALUE, "NULL data pointer");
+  for (int i = 0; i < 5; ++i)
+    if (!outs[i]) return fail(ST_ERR_VALUE, "NULL output plane %d", i);
+  if (h->order == 8 && v->order == 8) {
+    for (const Enc5Entry& e : kEnc5)
+      if (e.dtype == dtype && e.h == v->n && e.w == h->n) {
+        double cv[64], ch[64];
+        for (int r = 0; r < 8; ++r)
+          for (int j = 0; j < 8; ++j) {
+            cv[r * 8 + j] = v->mat[r * v->n + j];
+            ch[r * 8 + j] = h->mat[r * h->n + j];
+          }
+        return e.fn(x, outs, nblk, cv, ch, st);
+      }
+  }
+  // general sub-block orders / shapes: five fused 2-D transforms
+  std::vector<double> h8, v8;
+  chessboard(h, h8);
+  chessboard(v, v8);
+  dctadj_axis h7 = *h, v7 = *v, hd = *h, vd = *v, h8a = *h, v8a = *v;
+  hd.adj = vd.adj = DCTADJ_ADJ_NONE;
+  h8a.mat = h8.data();
+  v8a.mat = v8.data();
+  const dctadj_axis* hs[5] = {&hd, &h7, &h8a, &h7, &h8a};
+  const dctadj_axis* vs[5] = {&vd, &v7, &v7, &v8a, &v8a};
+  for (int i = 0; i < 5; ++i)
+    if ((rc = run_2d(hs[i], vs[i], x, outs[i], nblk, dtype, false, MODE_LINEAR, MODE_LINEAR, 0, 0,
+                     0, st)))
+      return rc;
+  return ST_OK;
+}
+
 // ------------------------------------------------------------- mixed batches
 }  // namespace dctadj
 
@@ -809,6 +924,11 @@ int dctadj_copy_tiles(const void* x, void* y, int64_t nblk, int32_t h, int32_t w
   L.a.out = y;
   L.a.rows = nblk * h;
   return L.k->fn(L.a);
+}
+
+int dctadj_encoder_eval(const dctadj_axis* h, const dctadj_axis* v, const void* x,
+                        void* const* planes, int64_t nblk, int32_t dtype, void* stream) {
+  return run_enc5(h, v, x, planes, nblk, dtype, S(stream));
 }
 
 int dctadj_mixed_create(const int64_t* offsets, const int32_t* h_index, const int32_t* v_index,

@@ -377,3 +377,95 @@ def mixed_forward(batch: MixedBatch, table, x):
 
 def mixed_inverse(batch: MixedBatch, table, y):
     return _mixed("dctadj_mixed_inverse", batch, table, y)
+
+
+# ---------------------------------------------------------------- encoder evaluation
+ENCODER_KEYS = (("dct2", "dct2"), ("dst7", "dst7"), ("dct8", "dst7"), ("dst7", "dct8"),
+                ("dct8", "dct8"))
+
+
+@dataclass(frozen=True)
+class EncoderContext:
+    """Sub-block DST-7 post-adjustments for both axes of a block; the DCT-8
+    counterparts follow from the chessboard relation (reference
+    pipeline.py:202-233)."""
+
+    horizontal: AdjustmentMatrix | None = None
+    vertical: AdjustmentMatrix | None = None
+
+    def require(self, width: int, height: int) -> tuple[AdjustmentMatrix, AdjustmentMatrix]:
+        if self.horizontal is None or self.vertical is None:
+            raise ConfigurationError(
+                "simultaneous evaluation needs sub-block adjustments for both dimensions")
+        for adj, size, name in ((self.horizontal, width, "horizontal"),
+                                (self.vertical, height, "vertical")):
+            if adj.pattern.kind is not PatternKind.SUBBLOCK:
+                raise ConfigurationError(f"{name} adjustment must be a sub-block design")
+            if adj.pattern.size != size:
+                raise ConfigurationError(
+                    f"{name} adjustment is for size {adj.pattern.size}, block needs {size}")
+            if adj.side is not Side.POST or adj.base is not TransformKind.DCT2 \
+                    or adj.target is not TransformKind.DST7:
+                raise ConfigurationError(f"{name} adjustment must be post-side dct2 -> dst7")
+        return self.horizontal, self.vertical
+
+
+def simultaneous_encoder_eval(block, ctx: EncoderContext) -> dict:
+    """The five encoder transform candidates of each residual block, keyed
+    (horizontal, vertical): ("dct2","dct2") and the four DST-7/DCT-8 pairs.
+    One fused kernel: one read, one shared 2-D DCT-2, five planes written;
+    coefficients outside the first 8 rows and columns are bit-identical across
+    the five outputs (reference pipeline.py:256-293)."""
+    t, as_np = _device.to_device(block)
+    single = t.dim() == 2
+    if t.dim() not in (2, 3):
+        raise ShapeError(f"expected a 2-D block or a batch of blocks, got ndim={t.dim()}")
+    blk = t.reshape(1, *t.shape) if single else t
+    height, width = int(blk.shape[1]), int(blk.shape[2])
+    _check_fast_size(width)
+    _check_fast_size(height)
+    h_adj, v_adj = ctx.require(width, height)
+    th, tv = make_adjusted_transform(h_adj), make_adjusted_transform(v_adj)
+    outs = [_device.empty_like(blk) for _ in ENCODER_KEYS]
+    ptrs = (ctypes.c_void_p * 5)(*[o.data_ptr() for o in outs])
+    (axh, _kh), (axv, _kv) = th.axis(), tv.axis()
+    _lib.call("dctadj_encoder_eval", ctypes.byref(axh), ctypes.byref(axv), blk.data_ptr(),
+              ptrs, blk.shape[0], _device.dtype_code(blk), _device.stream_handle())
+    res = {}
+    for key, o in zip(ENCODER_KEYS, outs):
+        o = _device.from_device(o, as_np)
+        res[key] = o[0] if single else o
+    return res
+
+
+def naive_encoder_eval(block, ctx: EncoderContext) -> dict:
+    """The same five outputs as independent dense separable transforms (the
+    comparison path, reference pipeline.py:296-323): five fused 2-D kernels
+    with the exact H = C B of each axis as a dense matrix."""
+    from .design import dct8_adjustment_from_dst7, pattern_schedule_template, SparsityPattern
+    t, as_np = _device.to_device(block)
+    single = t.dim() == 2
+    blk = t.reshape(1, *t.shape) if single else t
+    height, width = int(blk.shape[1]), int(blk.shape[2])
+    h_adj, v_adj = ctx.require(width, height)
+
+    def dense(adj):
+        h = dense_matrix(make_adjusted_transform(adj))
+        n = h.shape[0]
+        rec = AdjustmentMatrix(SparsityPattern.dense(n), Side.POST, TransformKind.DCT2,
+                               adj.target, pattern_schedule_template(SparsityPattern.dense(n)),
+                               h @ build_transform(TransformKind.DCT2, n).entries.T)
+        return make_adjusted_transform(rec)
+
+    def ident(n):
+        from .design import identity_adjustment
+        return make_adjusted_transform(identity_adjustment(
+            SparsityPattern.subblock(1, n), Side.POST, TransformKind.DCT2, TransformKind.DCT2))
+
+    hs = {"dct2": ident(width), "dst7": dense(h_adj), "dct8": dense(dct8_adjustment_from_dst7(h_adj))}
+    vs = {"dct2": ident(height), "dst7": dense(v_adj), "dct8": dense(dct8_adjustment_from_dst7(v_adj))}
+    res = {}
+    for key in ENCODER_KEYS:
+        o = _device.from_device(forward_adjusted_2d(hs[key[0]], vs[key[1]], blk), as_np)
+        res[key] = o[0] if single else o
+    return res

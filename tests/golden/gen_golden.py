@@ -179,5 +179,17 @@ out["c5/y"] = fwd2(post7[32], post7[32], np.ascontiguousarray(blocks))
 t7 = build_transform(TransformKind.DST7, 32).entries
 out["c5/y_exact"] = np.einsum("ij,bjk,lk->bil", t7, blocks, t7)
 
+# simultaneous five-output encoder evaluation (pipeline.py:256-323)
+from dctadjust.pipeline import EncoderContext, simultaneous_encoder_eval  # noqa: E402
+KEYS = (("dct2", "dct2"), ("dst7", "dst7"), ("dct8", "dst7"), ("dst7", "dct8"), ("dct8", "dct8"))
+for tag, (hn, vn) in {"32x32": (32, 32), "32x64": (64, 32), "16x16": (16, 16)}.items():
+    ctx = EncoderContext(horizontal=design(f"sub8_post_dct2_dst7_n{hn}"),
+                         vertical=design(f"sub8_post_dct2_dst7_n{vn}"))
+    blocks = rng.standard_normal((3, vn, hn)) * 16.0
+    out[f"enc5/{tag}/x"] = blocks
+    res = [simultaneous_encoder_eval(b, ctx) for b in blocks]
+    for k in KEYS:
+        out[f"enc5/{tag}/{k[0]}_{k[1]}"] = np.stack([r[k] for r in res])
+
 np.savez_compressed(HERE / "golden.npz", **out)
 print(f"wrote {len(out)} arrays, {(HERE / 'golden.npz').stat().st_size / 1e6:.2f} MB")

@@ -392,3 +392,38 @@ def test_mixed_batch_shuffled_offsets_and_errors():
         pipeline.MixedBatch([0], [2], [2], sizes, 512)         # block overruns the buffer
     with pytest.raises(ShapeError):
         pipeline.mixed_forward(batch, table[:2], dev(x))
+
+
+# ---------------------------------------------------------------- encoder evaluation (Table 1 "Multiple")
+@pytest.mark.parametrize("tag,hn,vn", [("32x32", 32, 32), ("32x64", 64, 32), ("16x16", 16, 16)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_encoder_eval_matches_reference(golden, tag, hn, vn, dtype):
+    ctx = pipeline.EncoderContext(horizontal=matio.load_designed(f"sub8_post_dct2_dst7_n{hn}"),
+                                  vertical=matio.load_designed(f"sub8_post_dct2_dst7_n{vn}"))
+    x = dev(golden[f"enc5/{tag}/x"], dtype)
+    res = pipeline.simultaneous_encoder_eval(x, ctx)
+    tol = F32_TOL if dtype == torch.float32 else F64_TOL
+    assert set(res) == set(pipeline.ENCODER_KEYS)
+    for k, v in res.items():
+        assert rel_err(v.cpu().numpy(), golden[f"enc5/{tag}/{k[0]}_{k[1]}"]) < tol, k
+    ref = res[("dct2", "dct2")]
+    for k, v in res.items():  # untouched coefficients bit-identical (test_pipeline.py:235-241)
+        assert torch.equal(v[:, 8:, 8:], ref[:, 8:, 8:]), k
+    naive = pipeline.naive_encoder_eval(x, ctx)
+    for k in res:
+        assert rel_err(res[k].cpu().numpy(), naive[k].cpu().numpy().astype(np.float64)) < tol, k
+
+
+def test_encoder_eval_errors_and_numpy_block():
+    ctx = pipeline.EncoderContext()
+    with pytest.raises(ConfigurationError):
+        pipeline.simultaneous_encoder_eval(np.zeros((32, 32)), ctx)
+    band = matio.load_designed("band6_pre_dst3_dst7_n32")
+    with pytest.raises(ConfigurationError):
+        pipeline.simultaneous_encoder_eval(np.zeros((32, 32)),
+                                           pipeline.EncoderContext(band, band))
+    s32 = matio.load_designed("sub8_post_dct2_dst7_n32")
+    with pytest.raises(ConfigurationError):
+        pipeline.simultaneous_encoder_eval(np.zeros((64, 64)), pipeline.EncoderContext(s32, s32))
+    out = pipeline.simultaneous_encoder_eval(np.zeros((32, 32)), pipeline.EncoderContext(s32, s32))
+    assert len(out) == 5 and all(np.array_equal(v, np.zeros((32, 32))) for v in out.values())

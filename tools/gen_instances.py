@@ -41,6 +41,9 @@ def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False
     if two_d:
         # rows: P*H >= 32; packed column pairs (fp32): P*W >= 64
         p = max(1, 32 // h, (64 // w) if dtype == "float" else 32 // w)
+    if two_d and (rc & 15) == DENSE:
+        # the dense comparison path is FMA-bound: many warps, scalar lanes
+        return max(1, 32 // h, 32 // w), 8, 3, False
     small32 = two_d and dtype == "float" and h * w <= 1024
     band_inv = col_first and (rc >> 8) in (4, 6) and (rc & 15) != SUB and ((rc >> 4) & 15) in (BAND, GIVENS)
     if small32:
@@ -48,8 +51,8 @@ def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False
             p, ng, s, pr = max(p, 4 * 1024 // (h * w)), 2, 3, True
         else:
             p, ng, s, pr = max(p, 2 * 1024 // (h * w)), 4, 4, not col_first
-        if (p * h) % 64:
-            pr = False
+        if (p * h) % 64 or (rc & 15) == DENSE:
+            pr = False  # dense rows read shared-memory coefficients: keep scalar FFMA
         return p, ng, s, pr
     tile = p * h * w * es
     stage = -(-tile // 1024) * 1024
@@ -111,8 +114,8 @@ def two_d_pairs():
 
 def pair_flags(dt, h, w, p, rc, cc):
     """Default packing: fp32 column pairs (FFMA2) when a column op exists and
-    the super-tile has >= 64 columns; rows stay scalar."""
-    if dt != "float" or cc == ID:
+    the super-tile has >= 64 columns (not for the dense comparison path)."""
+    if dt != "float" or cc == ID or (cc & 15) == DENSE:
         return (False, False)
     return (False, (p * w) % 64 == 0)
 
