@@ -236,3 +236,11 @@ def test_brickwall_detection_rejects_other_schedules():
     a = matio.load_designed("band6_pre_dst3_dst7_n32")
     odd = GivensSchedule(32, a.schedule.layers[:-1])  # one layer short
     assert brickwall_angles(replace(a, schedule=odd, pattern=SparsityPattern.band(6, 32))) is None
+
+
+def test_library_resolves_all_symbols_eagerly():
+    """RTLD_NOW: a stale or partial build (missing instantiation objects) fails here."""
+    import os
+    if not _lib.LIB_PATH.exists():
+        pytest.skip("libdctadj.so not built")
+    ctypes.CDLL(str(_lib.LIB_PATH), mode=os.RTLD_NOW)

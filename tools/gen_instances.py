@@ -12,7 +12,7 @@ from __future__ import annotations
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1] / "paper_2505_23618_b200" / "csrc" / "gen"
-NSHARDS = 12
+NSHARDS = 24
 
 NONE, DCT2, IDCT2, DST3, IDST3, BAND, SUB, DENSE, GIVENS = range(9)
 
@@ -42,8 +42,16 @@ def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False
         # rows: P*H >= 32; packed column pairs (fp32): P*W >= 64
         p = max(1, 32 // h, (64 // w) if dtype == "float" else 32 // w)
     if two_d and (rc & 15) == DENSE:
-        # the dense comparison path is FMA-bound: many warps, scalar lanes
-        return max(1, 32 // h, 32 // w), 8, 3, False
+        # the dense comparison path is FMA-bound: many warps, scalar lanes; the
+        # two dense matrices sit in shared memory beside the rings (<= 200 KB)
+        p = max(1, 32 // h, 32 // w)
+        stage = -(-(p * h * w * es) // 1024) * 1024
+        dense = (h * h + w * w) * es
+        for s in (3, 2):
+            ng = min(8, (200 * 1024 - dense) // (s * stage))
+            if ng >= 1:
+                return p, ng, s, False
+        raise ValueError(f"dense {h}x{w} {dtype} does not fit shared memory")
     small32 = two_d and dtype == "float" and h * w <= 1024
     band_inv = col_first and (rc >> 8) in (4, 6) and (rc & 15) != SUB and ((rc >> 4) & 15) in (BAND, GIVENS)
     if small32:
@@ -146,6 +154,17 @@ def instances():
             for rc, cc, cf in two_d_pairs():
                 p, ng, s, pr = tile_config(dt, h, w, True, cf, rc)
                 out.append((dt, h, w, p, rc, cc, cf, 0, 0, ng, s, pr))
+    # dense composite on every shape: the fallback that makes any (H, W) and any
+    # per-axis op combination available as one fused 2-D kernel
+    have = {(x[0], x[1], x[2], x[4], x[5], x[6]) for x in out}
+    for dt in DTYPES:
+        for h in (4, 8, 16, 32, 64):
+            for w in (4, 8, 16, 32, 64):
+                for cf in (False, True):
+                    if (dt, h, w, code(DENSE), code(DENSE), cf) in have:
+                        continue
+                    p, ng, s, pr = tile_config(dt, h, w, True, cf, code(DENSE))
+                    out.append((dt, h, w, p, code(DENSE), code(DENSE), cf, 0, 0, ng, s, pr))
     # frame tiling (config 5): 32x32 fp32, frames in / blocks out and back
     for rc, cc, cf in two_d_pairs():
         if rc == code(DCT2) or (rc >> 8) == 4:
