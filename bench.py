@@ -180,6 +180,7 @@ class Workload:
     e2e = None                   # callable for one end-to-end step, or None
     e2e_bytes = (0, 0)
     extra: dict = {}
+    kernels_per_step = None      # device kernels launched per step (default: one per launch)
 
     def gate(self) -> float:
         raise NotImplementedError
@@ -303,10 +304,15 @@ class Mixed(Workload):
             _lib.check(lib.dctadj_mixed_inverse(plan, self.axes, self.y.data_ptr(), self.xr.data_ptr(), 0, st))
 
         self.launches = [("mixed_forward", fwd), ("mixed_inverse", inv)]
+        self.kernels_per_step = 2 * len(self.batch_classes(h_index, v_index))
         self.h_index, self.v_index = h_index, v_index
         self.extra = {"blocks_per_gpu": nblk, "coefficients_per_gpu": total,
                       "classes": int(len(np.unique(h_index * 4 + v_index))),
                       "l2": f"inputs {total * 4 / 1e6:.0f} MB per GPU > 126 MB L2; no flush"}
+
+    @staticmethod
+    def batch_classes(h_index, v_index):
+        return np.unique(np.asarray(h_index) * 4 + np.asarray(v_index))
 
     def gate(self):
         from oracle import oracle as O
@@ -565,7 +571,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                  "h2d_bytes_per_step": w.e2e_bytes[0], "d2h_bytes_per_step": w.e2e_bytes[1],
                  "api": "forward_adjusted_2d_host / inverse_adjusted_2d_host (C-ABI *_2d_host)"}
                 if e2e_s else None),
-        "gpu_launches": args.steps * nl,
+        "gpu_launches": args.steps * (w.kernels_per_step or nl),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:

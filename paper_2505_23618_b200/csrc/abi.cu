@@ -703,6 +703,12 @@ struct dctadj_mixed {
   int64_t nblk = 0;
   int64_t* all = nullptr;  // device
   int device = 0;
+  // class kernels run concurrently on NSTREAM streams forked from the caller's
+  // stream (their persistent grids fill each other's tails)
+  static constexpr int NSTREAM = 4;
+  cudaStream_t aux[NSTREAM] = {};
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t join[NSTREAM] = {};
 };
 
 namespace dctadj {
@@ -720,17 +726,21 @@ static int run_mixed(const dctadj_mixed* plan, const dctadj_axis* table, const v
   }
   if (plan->nblk == 0) return ST_OK;
   if (!x || !y) return fail(ST_ERR_VALUE, "NULL data pointer");
+  DA_CUDA(cudaEventRecord(plan->fork, st));
+  for (int i = 0; i < dctadj_mixed::NSTREAM; ++i) DA_CUDA(cudaStreamWaitEvent(plan->aux[i], plan->fork, 0));
+  int ci = 0;
   for (const auto& c : plan->classes) {
+    cudaStream_t cs = plan->aux[ci++ % dctadj_mixed::NSTREAM];
     const dctadj_axis* h = &table[c.h_index];
     const dctadj_axis* v = &table[c.v_index];
     AxisPlan ph, pv;
     if ((rc = plan_axis(h, inverse, false, &ph)) || (rc = plan_axis(v, inverse, false, &pv))) return rc;
     Launch L;
-    rc = prepare(L, ph, &pv, dtype, v->n, h->n, inverse, MODE_GATHER, MODE_GATHER, st);
+    rc = prepare(L, ph, &pv, dtype, v->n, h->n, inverse, MODE_GATHER, MODE_GATHER, cs);
     if (rc == ST_ERR_UNSUPPORTED) {
       if ((rc = plan_axis(h, inverse, true, &ph)) || (rc = plan_axis(v, inverse, true, &pv))) return rc;
       L = Launch();
-      rc = prepare(L, ph, &pv, dtype, v->n, h->n, inverse, MODE_GATHER, MODE_GATHER, st);
+      rc = prepare(L, ph, &pv, dtype, v->n, h->n, inverse, MODE_GATHER, MODE_GATHER, cs);
       if (rc == ST_ERR_UNSUPPORTED)
         return fail(rc, "no gather kernel for %dx%d blocks, dtype %d", v->n, h->n, dtype);
     }
@@ -741,8 +751,12 @@ static int run_mixed(const dctadj_mixed* plan, const dctadj_axis* table, const v
     L.a.offsets = c.offsets;
     L.a.gather_blocks = c.count;
     rc = L.k->fn(L.a);
-    int rc2 = finish(L, st);
+    int rc2 = finish(L, cs);
     if (rc || rc2) return rc ? rc : rc2;
+  }
+  for (int i = 0; i < dctadj_mixed::NSTREAM; ++i) {
+    DA_CUDA(cudaEventRecord(plan->join[i], plan->aux[i]));
+    DA_CUDA(cudaStreamWaitEvent(st, plan->join[i], 0));
   }
   return ST_OK;
 }
@@ -984,6 +998,20 @@ int dctadj_mixed_create(const int64_t* offsets, const int32_t* h_index, const in
       const size_t c = static_cast<size_t>(hi) * ntable + vi;
       if (count[c]) plan->classes.push_back({hi, vi, count[c], plan->all + start[c]});
     }
+  // largest classes first (longest-processing-time order across the streams)
+  std::stable_sort(plan->classes.begin(), plan->classes.end(),
+                   [&](const dctadj_mixed::Class& a, const dctadj_mixed::Class& b) {
+                     return a.count * plan->sizes[a.h_index] * plan->sizes[a.v_index] >
+                            b.count * plan->sizes[b.h_index] * plan->sizes[b.v_index];
+                   });
+  bool ok = cudaEventCreateWithFlags(&plan->fork, cudaEventDisableTiming) == cudaSuccess;
+  for (int i = 0; ok && i < dctadj_mixed::NSTREAM; ++i)
+    ok = cudaStreamCreateWithFlags(&plan->aux[i], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&plan->join[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    dctadj_mixed_destroy(plan);
+    return fail(ST_ERR_CUDA, "mixed plan streams: %s", cudaGetErrorString(cudaGetLastError()));
+  }
   *out = plan;
   return ST_OK;
 }
@@ -998,6 +1026,14 @@ int dctadj_mixed_inverse(const dctadj_mixed* plan, const dctadj_axis* table, con
 }
 int dctadj_mixed_destroy(dctadj_mixed* plan) {
   if (!plan) return ST_OK;
+  for (int i = 0; i < dctadj_mixed::NSTREAM; ++i) {
+    if (plan->aux[i]) {
+      cudaStreamSynchronize(plan->aux[i]);
+      cudaStreamDestroy(plan->aux[i]);
+    }
+    if (plan->join[i]) cudaEventDestroy(plan->join[i]);
+  }
+  if (plan->fork) cudaEventDestroy(plan->fork);
   if (plan->all) cudaFree(plan->all);
   delete plan;
   return ST_OK;

@@ -13,10 +13,19 @@ from paper_2505_23618_b200 import _lib, workloads  # noqa: E402
 
 EXTRA = {"pre32": ("pre32", 65536, 32, "f32", lambda: bench._pre(32, "dst7"), "c2_inputs", True)}
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-wl, nblk, n_, dt_, make, inputs, inverse = EXTRA.get(name) or bench.UNIFORM[name]
-cfg = {"h": n_, "w": n_}
-th = tv = make()
-x = getattr(workloads, inputs)("cuda", nblk)
+if name.startswith("shape"):  # shape<side>_<H>x<W>: uniform blocks of one C3 class
+    side, hw = name[5:].split("_")
+    H, W = map(int, hw.split("x"))
+    mk = bench._pre if side == "pre" else bench._post
+    th, tv = mk(W, "dst7"), mk(H, "dst7")
+    nblk = (1 << 26) // (H * W)
+    cfg = {"h": H, "w": W}
+    x = workloads.ar1_blocks(nblk, H, W, 0.9, 16.0, 3)
+else:
+    wl, nblk, n_, dt_, make, inputs, inverse = EXTRA.get(name) or bench.UNIFORM[name]
+    cfg = {"h": n_, "w": n_}
+    th = tv = make()
+    x = getattr(workloads, inputs)("cuda", nblk)
 y = torch.empty_like(x)
 xr = torch.empty_like(x)
 lib = _lib.load()
