@@ -73,7 +73,8 @@ int make_map(CUtensorMap* map, const void* base, const LaunchArgs& a) {
 }
 
 template <typename T, int H, int W, int P, int RC, int CC, bool COL_FIRST, int IN_MODE,
-          int OUT_MODE, int NG, int S, bool PAIR_ROW = false, bool PAIR_COL = false, int CH = 0>
+          int OUT_MODE, int NG, int S, bool PAIR_ROW = false, bool PAIR_COL = false, int CH = 0,
+          int NW = 1>
 int launch_tile(const LaunchArgs& a) {
   using L = TileLayout<T, H, W, P>;
   using RowOp = AxisOp<T, W, RC>;
@@ -113,7 +114,7 @@ int launch_tile(const LaunchArgs& a) {
   if (RowOp::NCOEF > 0) std::memcpy(prm.row.c, a.row_coef, sizeof(T) * RowOp::NCOEF);
   if (ColOp::NCOEF > 0) std::memcpy(prm.col.c, a.col_coef, sizeof(T) * ColOp::NCOEF);
 
-  auto kern = tile_kernel<T, H, W, P, RC, CC, COL_FIRST, IN_MODE, OUT_MODE, NG, S, PAIR_ROW, PAIR_COL, CH>;
+  auto kern = tile_kernel<T, H, W, P, RC, CC, COL_FIRST, IN_MODE, OUT_MODE, NG, S, PAIR_ROW, PAIR_COL, CH, NW>;
   const size_t dense_bytes =
       sizeof(T) * ((RowOp::kDense ? W * W : 0) + (ColOp::kDense ? H * H : 0));
   const size_t smem = 1024 + static_cast<size_t>(NG) * S * L::STAGEB + NG * S * 8 + dense_bytes;
@@ -128,7 +129,7 @@ int launch_tile(const LaunchArgs& a) {
       return ST_ERR_CUDA;
     }
     int nb = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NG * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NG * NW * 32, smem);
     if (e != cudaSuccess || nb < 1) {
       set_last_error("occupancy query failed (%s, %d blocks)", cudaGetErrorString(e), nb);
       return ST_ERR_CUDA;
@@ -140,7 +141,7 @@ int launch_tile(const LaunchArgs& a) {
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * blocks_per_sm;
   const int grid = static_cast<int>(want < cap ? want : cap);
 
-  kern<<<grid, NG * 32, smem, a.stream>>>(in_map, out_map, g, prm);
+  kern<<<grid, NG * NW * 32, smem, a.stream>>>(in_map, out_map, g, prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_last_error("tile_kernel launch: %s", cudaGetErrorString(e));

@@ -251,15 +251,15 @@ DA_DEV void scale_out(V (&v)[N]) {
   }
 }
 
-// Row pass: lane owns a row (PAIR: two rows, rho and rho + 32, packed as f2
+// Row pass: lane owns a row (PAIR: two rows, rho and rho + GT, packed as f2
 // lanes).  Rows are read/written as 16-byte chunks: conflict-free under the
 // swizzle (8 lanes of a phase hit 8 distinct chunk columns).
-template <typename T, int H, int W, int P, int RC, int GSQ, bool PAIR>
+template <typename T, int H, int W, int P, int RC, int GSQ, bool PAIR, int GT = 32>
 DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Coef& cf,
                      const T* dense) {
   using L = TileLayout<T, H, W, P>;
   constexpr int PER16 = 16 / sizeof(T);
-  constexpr int ROWS_PER_IT = PAIR ? 64 : 32;
+  constexpr int ROWS_PER_IT = PAIR ? 2 * GT : GT;
   static_assert(L::PH % ROWS_PER_IT == 0, "row pass must cover whole warps");
 #pragma unroll 1
   for (int it = 0; it < L::PH / ROWS_PER_IT; ++it) {
@@ -289,7 +289,7 @@ DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Co
 #pragma unroll
       for (int q = 0; q < W / 4; ++q) {
         const float4 a = *reinterpret_cast<const float4*>(buf + L::addr(rho, q * 16));
-        const float4 b = *reinterpret_cast<const float4*>(buf + L::addr(rho + 32, q * 16));
+        const float4 b = *reinterpret_cast<const float4*>(buf + L::addr(rho + GT, q * 16));
         v[4 * q + 0].v = make_float2(a.x, b.x);
         v[4 * q + 1].v = make_float2(a.y, b.y);
         v[4 * q + 2].v = make_float2(a.z, b.z);
@@ -301,7 +301,7 @@ DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Co
       for (int q = 0; q < W / 4; ++q) {
         *reinterpret_cast<float4*>(buf + L::addr(rho, q * 16)) =
             make_float4(v[4 * q].v.x, v[4 * q + 1].v.x, v[4 * q + 2].v.x, v[4 * q + 3].v.x);
-        *reinterpret_cast<float4*>(buf + L::addr(rho + 32, q * 16)) =
+        *reinterpret_cast<float4*>(buf + L::addr(rho + GT, q * 16)) =
             make_float4(v[4 * q].v.y, v[4 * q + 1].v.y, v[4 * q + 2].v.y, v[4 * q + 3].v.y);
       }
     }
@@ -310,11 +310,11 @@ DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Co
 
 // Column pass: lane owns a column (PAIR: two adjacent columns read as one
 // 8-byte word, packed as f2 lanes).  Conflict-free under the swizzle.
-template <typename T, int H, int W, int P, int CC, int GSQ, bool PAIR>
+template <typename T, int H, int W, int P, int CC, int GSQ, bool PAIR, int GT = 32>
 DA_DEV void col_pass(uint8_t* buf, int lane, const typename AxisOp<T, H, CC>::Coef& cf,
                      const T* dense) {
   using L = TileLayout<T, H, W, P>;
-  constexpr int COLS_PER_IT = PAIR ? 64 : 32;
+  constexpr int COLS_PER_IT = PAIR ? 2 * GT : GT;
   static_assert((P * W) % COLS_PER_IT == 0, "column pass must cover whole warps");
 #pragma unroll 1
   for (int it = 0; it < (P * W) / COLS_PER_IT; ++it) {
@@ -345,24 +345,37 @@ DA_DEV void col_pass(uint8_t* buf, int lane, const typename AxisOp<T, H, CC>::Co
   }
 }
 
-// NG warps per CTA, each with an S-stage ring.
+// NG groups of NW warps per CTA; each group owns an S-stage ring and works one
+// super-tile at a time (NW > 1: the rows / columns of a tile are split across
+// the group's warps, synchronised by a named barrier).
+template <int NW>
+DA_DEV void group_sync(int grp) {
+  if constexpr (NW == 1)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(NW * 32) : "memory");
+}
+
 template <typename T, int H, int W, int P, int RC, int CC, bool COL_FIRST, int IN_MODE,
-          int OUT_MODE, int NG, int S, bool PAIR_ROW = false, bool PAIR_COL = false, int CH = 0>
-__global__ void __launch_bounds__(NG * 32)
+          int OUT_MODE, int NG, int S, bool PAIR_ROW = false, bool PAIR_COL = false, int CH = 0,
+          int NW = 1>
+__global__ void __launch_bounds__(NG * NW * 32)
     tile_kernel(const __grid_constant__ CUtensorMap in_map,
                 const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
                 const __grid_constant__ KParams<T, W, H, RC, CC> prm) {
   using L = TileLayout<T, H, W, P>;
   using RowOp = AxisOp<T, W, RC>;
   using ColOp = AxisOp<T, H, CC>;
-  static_assert(ColOp::kIdentity || (P * W) % 32 == 0, "column pass must cover whole warps");
+  constexpr int GT = NW * 32;
+  static_assert(NG * NW <= 32 && (NW == 1 || NG <= 15), "named barriers 1..15");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // dynamic smem is only guaranteed 16-byte aligned: round up to 1024 for the swizzle atom
   // (pointer arithmetic, not an integer round trip, keeps the shared address space)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * S * L::STAGEB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NG * S * L::STAGEB) + warp * S;
+  // `lane`: thread index within the group (0 .. NW*32-1)
+  const int grp = threadIdx.x / GT, lane = threadIdx.x % GT;
+  uint8_t* ring = smem + grp * S * L::STAGEB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NG * S * L::STAGEB) + grp * S;
   T* dense_base = reinterpret_cast<T*>(smem + NG * S * L::STAGEB + NG * S * 8);
   T* dense_row = dense_base;
   T* dense_col = dense_base + (RowOp::kDense ? W * W : 0);
@@ -370,11 +383,11 @@ __global__ void __launch_bounds__(NG * 32)
   if constexpr (RowOp::kDense || ColOp::kDense) {
     if constexpr (RowOp::kDense) {
       const T* src = static_cast<const T*>(geom.dense_row);
-      for (int i = threadIdx.x; i < W * W; i += NG * 32) dense_row[i] = src[i];
+      for (int i = threadIdx.x; i < W * W; i += NG * GT) dense_row[i] = src[i];
     }
     if constexpr (ColOp::kDense) {
       const T* src = static_cast<const T*>(geom.dense_col);
-      for (int i = threadIdx.x; i < H * H; i += NG * 32) dense_col[i] = src[i];
+      for (int i = threadIdx.x; i < H * H; i += NG * GT) dense_col[i] = src[i];
     }
     __syncthreads();
   }
@@ -383,24 +396,24 @@ __global__ void __launch_bounds__(NG * 32)
 #pragma unroll
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    if (warp == 0) {
+    if (grp == 0) {
       prefetch_map(&in_map);
       prefetch_map(&out_map);
     }
   }
-  __syncwarp();
+  group_sync<NW>(grp);
 
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * NG + warp;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * NG + grp;
   const int64_t gstride = static_cast<int64_t>(gridDim.x) * NG;
   const int64_t ntiles = geom.ntiles;
 
   constexpr bool GATHER = IN_MODE == MODE_GATHER;
   static_assert(GATHER == (OUT_MODE == MODE_GATHER), "gather mode is in+out");
-  static_assert(!GATHER || P <= 32, "one lane per gathered block");
+  static_assert(!GATHER || P <= GT, "one thread per gathered block");
   // GATHER: the offsets of the blocks in flight (stage-major) and a register
   // prefetch of the next refill's offsets, one lane per block
   __shared__ int64_t goffs[GATHER ? NG * S * P : 1];
-  int64_t* my_offs = goffs + (GATHER ? warp * S * P : 0);
+  int64_t* my_offs = goffs + (GATHER ? grp * S * P : 0);
   int64_t pref = 0;
 
   if constexpr (!GATHER) {
@@ -423,7 +436,7 @@ __global__ void __launch_bounds__(NG * 32)
       if (t < ntiles) {
         const int nb = tile_blocks<P, IN_MODE>(t, geom);
         if (lane == 0) mbar_arrive_expect_tx(&bars[s], L::TILEB / P * nb);
-        __syncwarp();
+        group_sync<NW>(grp);
         const int64_t off = lane < nb ? geom.offsets[t * P + lane] : 0;
         if (lane < P) my_offs[s * P + lane] = off;
         gather_io<T, H, W, P>(true, ring + s * L::STAGEB, &in_map, &bars[s], lane, nb, off);
@@ -442,21 +455,23 @@ __global__ void __launch_bounds__(NG * 32)
     constexpr int GSQ = RowOp::kGainSq * ColOp::kGainSq;
     if constexpr (!COL_FIRST) {
       if constexpr (!RowOp::kIdentity) {
-        row_pass<T, H, W, P, RC, ColOp::kIdentity ? GSQ : 1, PAIR_ROW>(buf, lane, prm.row, dense_row);
-        if constexpr (!ColOp::kIdentity) __syncwarp();
+        row_pass<T, H, W, P, RC, ColOp::kIdentity ? GSQ : 1, PAIR_ROW, GT>(buf, lane, prm.row,
+                                                                          dense_row);
+        if constexpr (!ColOp::kIdentity) group_sync<NW>(grp);
       }
       if constexpr (!ColOp::kIdentity)
-        col_pass<T, H, W, P, CC, GSQ, PAIR_COL>(buf, lane, prm.col, dense_col);
+        col_pass<T, H, W, P, CC, GSQ, PAIR_COL, GT>(buf, lane, prm.col, dense_col);
     } else {
       if constexpr (!ColOp::kIdentity) {
-        col_pass<T, H, W, P, CC, RowOp::kIdentity ? GSQ : 1, PAIR_COL>(buf, lane, prm.col, dense_col);
-        if constexpr (!RowOp::kIdentity) __syncwarp();
+        col_pass<T, H, W, P, CC, RowOp::kIdentity ? GSQ : 1, PAIR_COL, GT>(buf, lane, prm.col,
+                                                                          dense_col);
+        if constexpr (!RowOp::kIdentity) group_sync<NW>(grp);
       }
       if constexpr (!RowOp::kIdentity)
-        row_pass<T, H, W, P, RC, GSQ, PAIR_ROW>(buf, lane, prm.row, dense_row);
+        row_pass<T, H, W, P, RC, GSQ, PAIR_ROW, GT>(buf, lane, prm.row, dense_row);
     }
     fence_proxy_async_smem();
-    __syncwarp();
+    group_sync<NW>(grp);
     if constexpr (!GATHER) {
       if (lane == 0) {
         issue_tile_io<T, H, W, P, OUT_MODE, CH>(false, buf, &out_map, nullptr, t, geom,
@@ -487,7 +502,7 @@ __global__ void __launch_bounds__(NG * 32)
           bulk_wait_read<1>();
           const int nb = tile_blocks<P, IN_MODE>(tn, geom);
           if (lane == 0) mbar_arrive_expect_tx(&bars[sp], L::TILEB / P * nb);
-          __syncwarp();
+          group_sync<NW>(grp);
           if (lane < P) my_offs[sp * P + lane] = pref;
           gather_io<T, H, W, P>(true, ring + sp * L::STAGEB, &in_map, &bars[sp], lane, nb, pref);
           const int64_t tq = tn + gstride;  // prefetch the next refill's offsets
@@ -496,7 +511,7 @@ __global__ void __launch_bounds__(NG * 32)
         }
       }
     }
-    __syncwarp();
+    group_sync<NW>(grp);
     if (++s == S) {
       s = 0;
       phase ^= 1;

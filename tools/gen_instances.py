@@ -64,6 +64,12 @@ def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False
         return p, ng, s, pr
     tile = p * h * w * es
     stage = -(-tile // 1024) * 1024
+    if two_d and dtype == "float" and (h, w) == (64, 64):
+        givens = (rc & 15) == GIVENS or ((rc >> 4) & 15) == GIVENS
+        if givens or col_first:
+            # 64-point vectors: two warps per tile, scalar lanes, 12 warps/SM
+            # (the packed 64-column pass needs ~200 registers; measured faster)
+            return p, 6, 2, ("NW2",)
     if stage <= 2048:
         ng, s = 8, 4
     elif stage <= 4096:
@@ -134,8 +140,9 @@ def pair_flags(dt, h, w, p, rc, cc):
 EXPERIMENT = {
     (32, 32): [(4, 2, 3, True, True, 0), (2, 4, 4, True, True, 0), (4, 2, 3, False, True, 0),
                (2, 4, 4, False, True, 0)],
-    (64, 64): [(1, 4, 3, False, True, 0), (1, 6, 2, False, True, 0), (1, 8, 2, False, True, 0),
-               (1, 5, 2, False, True, 0)],
+    (64, 64): [(1, 6, 2, False, False, 0, 2), (1, 4, 3, False, False, 0, 2),
+               (1, 5, 2, False, False, 0, 2), (1, 3, 4, False, False, 0, 2),
+               (2, 3, 2, False, False, 0, 4), (2, 2, 3, False, False, 0, 4)],
 }
 EXPERIMENT_OPS = None  # filled below: the band-6 and sub-8 2-D ops
 
@@ -190,19 +197,26 @@ def instances():
     for inst in out:
         dt, h, w, p, rc, cc, cf, im, om, ng, s_, pr = inst
         _, pc = pair_flags(dt, h, w, p, rc, cc)
+        if pr == ("NW2",):  # two warps per tile, scalar lanes
+            final.append(inst[:11] + (False, False, 0, 0, 2))
+            continue
         final.append(inst[:11] + (pr and cc != ID, pc, 0, 0))
         if dt == "float" and (h, w) in EXPERIMENT and im == 0 and om == 0 and rc == cc \
                 and rc in (code(DCT2, SUB, 8), code(SUB, IDCT2, 8), code(GIVENS, DST3, 6),
                            code(IDST3, GIVENS, 6)):
-            for k, (pp, nng, ss, pr, pc, ch) in enumerate(EXPERIMENT[(h, w)], start=1):
-                final.append((dt, h, w, pp, rc, cc, cf, im, om, nng, ss, pr, pc, k, ch))
+            for k, ex in enumerate(EXPERIMENT[(h, w)], start=1):
+                pp, nng, ss, pr, pc, ch = ex[:6]
+                nw = ex[6] if len(ex) > 6 else 1
+                final.append((dt, h, w, pp, rc, cc, cf, im, om, nng, ss, pr, pc, k, ch, nw))
     return final
 
 
 def _targs(inst) -> str:
-    dt, h, w, p, rc, cc, cf, im, om, ng, s, pr, pc, var, ch = inst
+    dt, h, w, p, rc, cc, cf, im, om, ng, s, pr, pc, var, ch = inst[:15]
+    nw = inst[15] if len(inst) > 15 else 1
     b = lambda v: "true" if v else "false"  # noqa: E731
-    return f"{dt}, {h}, {w}, {p}, {rc}, {cc}, {b(cf)}, {im}, {om}, {ng}, {s}, {b(pr)}, {b(pc)}, {ch}"
+    return (f"{dt}, {h}, {w}, {p}, {rc}, {cc}, {b(cf)}, {im}, {om}, {ng}, {s}, {b(pr)}, {b(pc)}, "
+            f"{ch}, {nw}")
 
 
 def _write_if_changed(path: Path, text: str) -> None:
@@ -229,7 +243,7 @@ def main():
     decl = []
     rows = []
     for inst in insts:
-        dt, h, w, p, rc, cc, cf, im, om, ng, s, pr, pc, var, ch = inst
+        dt, h, w, p, rc, cc, cf, im, om, ng, s, pr, pc, var, ch = inst[:15]
         targs = _targs(inst)
         decl.append(f"extern template int launch_tile<{targs}>(const LaunchArgs&);")
         rows.append(f"  {{{DTYPES[dt]}, {h}, {w}, {rc}, {cc}, {int(cf)}, {im}, {om}, {var}, "
