@@ -138,9 +138,12 @@ def pair_flags(dt, h, w, p, rc, cc):
 # tuning variants (DCTADJ_VARIANT=k, k >= 1), per (H, W) of fp32 uniform 2-D kernels:
 # (P, NG, S, pair_rows, pair_cols, L2 hints); variant 0 is always the default build
 EXPERIMENT = {
-    (32, 32): [(4, 2, 3, True, True, 0), (2, 4, 4, True, True, 0), (4, 2, 3, False, True, 0),
+    ("double", 32, 32): [(1, 8, 2, False, False, 0, 1), (1, 2, 4, False, False, 0, 1),
+                         (2, 2, 2, False, False, 0, 2), (2, 3, 2, False, False, 0, 2),
+                         (2, 1, 4, False, False, 0, 2), (1, 12, 2, False, False, 0, 1)],
+    ("float", 32, 32): [(4, 2, 3, True, True, 0), (2, 4, 4, True, True, 0), (4, 2, 3, False, True, 0),
                (2, 4, 4, False, True, 0)],
-    (64, 64): [(1, 6, 2, False, False, 0, 2), (1, 4, 3, False, False, 0, 2),
+    ("float", 64, 64): [(1, 6, 2, False, False, 0, 2), (1, 4, 3, False, False, 0, 2),
                (1, 5, 2, False, False, 0, 2), (1, 3, 4, False, False, 0, 2),
                (2, 3, 2, False, False, 0, 4), (2, 2, 3, False, False, 0, 4)],
 }
@@ -201,10 +204,10 @@ def instances():
             final.append(inst[:11] + (False, False, 0, 0, 2))
             continue
         final.append(inst[:11] + (pr and cc != ID, pc, 0, 0))
-        if dt == "float" and (h, w) in EXPERIMENT and im == 0 and om == 0 and rc == cc \
+        if (dt, h, w) in EXPERIMENT and im == 0 and om == 0 and rc == cc \
                 and rc in (code(DCT2, SUB, 8), code(SUB, IDCT2, 8), code(GIVENS, DST3, 6),
                            code(IDST3, GIVENS, 6)):
-            for k, ex in enumerate(EXPERIMENT[(h, w)], start=1):
+            for k, ex in enumerate(EXPERIMENT[(dt, h, w)], start=1):
                 pp, nng, ss, pr, pc, ch = ex[:6]
                 nw = ex[6] if len(ex) > 6 else 1
                 final.append((dt, h, w, pp, rc, cc, cf, im, om, nng, ss, pr, pc, k, ch, nw))
