@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/dctadj.h"
+#include "dense_tc.cuh"
 #include "enc5.cuh"
 #include "launch.cuh"
 
@@ -433,6 +434,46 @@ static int primitive(int stage, const void* x, void* y, int64_t nvec, int n, int
   return run_1d(p, x, y, nvec, dtype, st);
 }
 
+// ------------------------------------------------------------- dense on tensor cores
+// DCTADJ_DENSE_TC=0 keeps the dense comparison path on the CUDA-core kernel
+static bool dense_tc_enabled() {
+  static bool v = [] {
+    const char* s = std::getenv("DCTADJ_DENSE_TC");
+    return !(s && s[0] == '0');
+  }();
+  return v;
+}
+
+template <int IN_MODE, int OUT_MODE>
+static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, int tiles_x) {
+  constexpr int S = 3;
+  Geom g{};
+  g.nblocks = nblocks;
+  g.ntiles = (nblocks + 3) / 4;
+  g.tiles_y = tiles_y;
+  g.tiles_x = tiles_x;
+  LaunchArgs la = a;
+  la.rows = nblocks * 32;
+  CUtensorMap in_map, out_map;
+  int rc = make_map<float, 32, 32, 4, IN_MODE>(&in_map, a.in, la);
+  if (!rc) rc = make_map<float, 32, 32, 4, OUT_MODE>(&out_map, a.out, la);
+  if (rc) return rc;
+  DenseTcParams prm{static_cast<const float*>(a.dense_row), static_cast<const float*>(a.dense_col)};
+  auto kern = dense_tc_kernel<S, IN_MODE, OUT_MODE>;
+  const size_t smem = 1024 + S * 16384 + 16384 + 16384 + (S + 1) * 8 + 16;
+  static int bps = 0;
+  if (!bps) {
+    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 128, smem));
+    if (bps < 1) return fail(ST_ERR_CUDA, "dense tensor-core kernel does not fit an SM");
+  }
+  const int64_t cap = static_cast<int64_t>(num_sms_cached()) * bps;
+  kern<<<static_cast<int>(std::min<int64_t>(g.ntiles, cap)), 128, smem, a.stream>>>(in_map, out_map,
+                                                                                    g, prm);
+  DA_CUDA(cudaGetLastError());
+  return ST_OK;
+}
+
 // ------------------------------------------------------------- 2-D / frames
 static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
                   int64_t nblk, int dtype, bool inverse, int in_mode, int out_mode,
@@ -449,6 +490,30 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
   if (!x || !y) return fail(ST_ERR_VALUE, "NULL data pointer");
   const int H = pv.n, W = ph.n;
   Launch L;
+  if (dtype == DT_F32 && H == 32 && W == 32 && ph.code == op_code(ST_DENSE) &&
+      pv.code == op_code(ST_DENSE) && dense_tc_enabled() && in_mode != MODE_GATHER) {
+    // the dense comparison path on the tensor cores (3xTF32 tcgen05, dense_tc.cuh)
+    if ((rc = upload_dense(ph, dtype, st, &L.dense_row)) || (rc = upload_dense(pv, dtype, st, &L.dense_col)))
+      return rc;
+    LaunchArgs a;
+    a.in = x;
+    a.out = y;
+    a.frames = frames;
+    a.frame_h = fh;
+    a.frame_w = fw;
+    a.dense_row = L.dense_row;
+    a.dense_col = L.dense_col;
+    a.stream = st;
+    const int ty = (fh + H - 1) / H, tx = fw / W;
+    if (in_mode == MODE_LINEAR && out_mode == MODE_LINEAR)
+      rc = launch_dense_tc<MODE_LINEAR, MODE_LINEAR>(a, nblk, 0, 0);
+    else if (in_mode == MODE_FRAME)
+      rc = launch_dense_tc<MODE_FRAME, MODE_LINEAR>(a, nblk, ty, tx);
+    else
+      rc = launch_dense_tc<MODE_LINEAR, MODE_FRAME>(a, nblk, ty, tx);
+    int rc2 = finish(L, st);
+    return rc ? rc : rc2;
+  }
   rc = prepare(L, ph, &pv, dtype, H, W, inverse, in_mode, out_mode, st);
   if (rc == ST_ERR_UNSUPPORTED) {
     // dense composite of both axes: one fused kernel per shape is always built
