@@ -446,7 +446,9 @@ static bool dense_tc_enabled() {
 
 template <int IN_MODE, int OUT_MODE>
 static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, int tiles_x) {
-  constexpr int S = 3;
+  // a stage is held from the tile's load until both GEMMs have read it (3 pipeline
+  // phases): S = 8 leaves 5 tiles (80 KB) of loads in flight per SM
+  constexpr int S = 8;
   Geom g{};
   g.nblocks = nblocks;
   g.ntiles = (nblocks + 3) / 4;
@@ -460,15 +462,20 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   if (rc) return rc;
   DenseTcParams prm{static_cast<const float*>(a.dense_row), static_cast<const float*>(a.dense_col)};
   auto kern = dense_tc_kernel<S, IN_MODE, OUT_MODE>;
-  const size_t smem = 1024 + S * 16384 + 16384 + 16384 + (S + 1) * 8 + 16;
+  const size_t smem = 1024 + S * 16384 + 3 * 16384 + 16384 + (S + 6) * 8 + 16;
   static int bps = 0;
   if (!bps) {
     DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 128, smem));
+    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, smem));
     if (bps < 1) return fail(ST_ERR_CUDA, "dense tensor-core kernel does not fit an SM");
+    bps = std::min(bps, 2);  // 256 TMEM columns per CTA, 512 per SM
+    if (trace_on())
+      std::fprintf(stderr, "[dctadj] dense_tc: %zu B smem, %d CTAs/SM\n", smem, bps);
   }
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * bps;
-  kern<<<static_cast<int>(std::min<int64_t>(g.ntiles, cap)), 128, smem, a.stream>>>(in_map, out_map,
+  kern<<<static_cast<int>(std::min<int64_t>(g.ntiles, cap)), 256, smem, a.stream>>>(in_map, out_map,
                                                                                     g, prm);
   DA_CUDA(cudaGetLastError());
   return ST_OK;

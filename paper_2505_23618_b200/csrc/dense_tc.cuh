@@ -21,11 +21,9 @@ namespace dctadj {
 
 namespace tc {
 
-DA_DEV uint32_t tf32_hi(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
+// tf32 "hi" part by truncation (low 13 mantissa bits cleared); x - hi is exact
+// in fp32, and the tensor core reads both as tf32 (3xTF32 split)
+DA_DEV uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
 // K-major SW128 UMMA smem descriptor (start address >> 4, LBO 16 B, SBO 1024 B,
 // version 1, layout SWIZZLE_128B); the tile base must be 1024-byte aligned.
@@ -53,6 +51,17 @@ DA_DEV void commit(uint64_t* bar) {
 }
 DA_DEV void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 DA_DEV void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+DA_DEV void ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 
 DA_DEV void ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -94,30 +103,40 @@ struct DenseTcParams {
   const float* dv;  // device 32x32: column-pass matrix
 };
 
-// S-stage TMA ring of 4-block super-tiles; one CTA = 4 warps = 128 TMEM lanes.
+// S-stage TMA ring of 4-block super-tiles; one CTA = 8 warps: warps w and w+4
+// share TMEM lane quadrant w%4 (tile rows 32(w%4) ..), each moving 16 of the 32
+// columns.
+// Three tiles are in flight per CTA (TMEM and `lo` buffers triple-buffered) so
+// each tensor-core GEMM hides behind a full phase of thread work:
+//   iteration k:  A(k)   split X_k into tf32 hi / lo, issue GEMM1(k)
+//                 C(k-2) wait GEMM2(k-2), TMEM -> Y tile, TMA store, refill
+//                 B(k-1) wait GEMM1(k-1), TMEM -> Z^T operand, issue GEMM2(k-1)
 template <int S, int IN_MODE, int OUT_MODE>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     dense_tc_kernel(const __grid_constant__ CUtensorMap in_map,
                     const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
                     const __grid_constant__ DenseTcParams prm) {
   using L = TileLayout<float, 32, 32, 4>;  // 128 rows x 128 B, SW128
   static_assert(L::TILEB == 16384 && L::STAGEB == 16384, "4 blocks of 32x32 fp32");
+  static_assert(S >= 4, "a stage is held from A(k) until C(k)");
+  constexpr int NSLOT = 3;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stages = smem;                       // S x 16 KB: X tile, then Z^T hi
-  uint8_t* lo = smem + S * 16384;               // 16 KB: X lo, then Z^T lo, then Y
-  uint8_t* bmat = lo + 16384;                   // 4 x 4 KB: Dh hi/lo, Dv hi/lo (32 rows)
+  uint8_t* lobuf = smem + S * 16384;            // NSLOT x 16 KB: X lo, then Z^T lo, then Y
+  uint8_t* bmat = lobuf + NSLOT * 16384;        // 4 x 4 KB: Dh hi/lo, Dv hi/lo (32 rows)
   uint8_t* dh_hi = bmat;
   uint8_t* dh_lo = bmat + 4096;
   uint8_t* dv_hi = bmat + 8192;
   uint8_t* dv_lo = bmat + 12288;
   uint64_t* full = reinterpret_cast<uint64_t*>(bmat + 16384);
-  uint64_t* mma_bar = full + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
+  uint64_t* bar1 = full + S;       // GEMM1 done, per slot
+  uint64_t* bar2 = bar1 + NSLOT;   // GEMM2 done, per slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar2 + NSLOT);
   const int tid = threadIdx.x, warp = tid >> 5;
 
   // constant operands: split Dh, Dv into tf32 hi / lo, K-major SW128 (32 rows)
-  for (int e = tid; e < 1024; e += 128) {
+  for (int e = tid; e < 1024; e += 256) {
     const int r = e >> 5, c = e & 31;
     const float h = prm.dh[e], v = prm.dv[e];
     const uint32_t hh = tc::tf32_hi(h), vh = tc::tf32_hi(v);
@@ -128,11 +147,14 @@ __global__ void __launch_bounds__(128)
   }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
-    mbar_init(mma_bar, 1);
+    for (int j = 0; j < NSLOT; ++j) {
+      mbar_init(&bar1[j], 1);
+      mbar_init(&bar2[j], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
                      smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -142,109 +164,119 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t d1 = tmem, d2 = tmem + 32;
-  const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+  const uint32_t quad = warp & 3, half = warp >> 2;
+  const uint32_t lane_addr = (quad * 32) << 16;
+  const uint32_t m = quad * 32 + (tid & 31);  // TMEM lane / tile row owned by this thread
+  const uint32_t c0 = half * 16;              // the 16 columns this thread moves
 
   const int64_t ntiles = geom.ntiles;
+  const int64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto tile_of = [&](int64_t k) { return blockIdx.x + k * gridDim.x; };
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      const int64_t t = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
-      if (t < ntiles) {
-        const int nb = tile_blocks<4, IN_MODE>(t, geom);
-        mbar_arrive_expect_tx(&full[s], 4096 * nb);
-        issue_tile_io<float, 32, 32, 4, IN_MODE>(true, stages + s * 16384, &in_map, &full[s], t,
-                                                 geom, nb);
-      }
+    for (int s = 0; s < S && s < mine; ++s) {
+      const int64_t t = tile_of(s);
+      const int nb = tile_blocks<4, IN_MODE>(t, geom);
+      mbar_arrive_expect_tx(&full[s], 4096 * nb);
+      issue_tile_io<float, 32, 32, 4, IN_MODE>(true, stages + s * 16384, &in_map, &full[s], t,
+                                               geom, nb);
     }
   }
-  int s = 0;
-  uint32_t phase = 0, mphase = 0;
-  const uint32_t m = tid;  // TMEM lane / tile row owned by this thread
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    uint8_t* x = stages + s * 16384;
-    mbar_wait(&full[s], phase);
-    if (tid == 0) bulk_wait_read<0>();  // the previous output tile (in `lo`) is stored
-    __syncthreads();
-    // split row m into tf32 hi (in place) and lo
+
+  for (int64_t k = 0; k < mine + 2; ++k) {
+    // ---- A(k): split X_k into tf32 hi (in place) and lo; GEMM1(k)
+    if (k < mine) {
+      const int slot = static_cast<int>(k % NSLOT);
+      uint8_t* x = stages + (k % S) * 16384;
+      uint8_t* lo = lobuf + slot * 16384;
+      mbar_wait(&full[k % S], static_cast<uint32_t>((k / S) & 1));
+      if (tid == 0) bulk_wait_read<0>();  // Y(k-3), stored from this lo buffer, is read
+      __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t o = tc::sw(m, q * 4);
-      float4 v = *reinterpret_cast<const float4*>(x + o);
-      uint4 h = make_uint4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
-      *reinterpret_cast<uint4*>(x + o) = h;
-      *reinterpret_cast<float4*>(lo + o) =
-          make_float4(v.x - __uint_as_float(h.x), v.y - __uint_as_float(h.y),
-                      v.z - __uint_as_float(h.z), v.w - __uint_as_float(h.w));
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t o = tc::sw(m, c0 + q * 4);
+        const float4 v = *reinterpret_cast<const float4*>(x + o);
+        const uint4 h =
+            make_uint4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
+        *reinterpret_cast<uint4*>(x + o) = h;
+        *reinterpret_cast<float4*>(lo + o) =
+            make_float4(v.x - __uint_as_float(h.x), v.y - __uint_as_float(h.y),
+                        v.z - __uint_as_float(h.z), v.w - __uint_as_float(h.w));
+      }
+      fence_proxy_async_smem();
+      tc::fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after();
+        tc::gemm3(tmem + 64 * slot, x, lo, dh_hi, dh_lo);
+        tc::commit(&bar1[slot]);
+      }
     }
-    fence_proxy_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    if (tid == 0) {
+    // ---- C(k-2): Y(k-2) from TMEM, store, refill its stage
+    if (k >= 2 && k - 2 < mine) {
+      const int64_t kp = k - 2;
+      const int ps = static_cast<int>(kp % NSLOT);
+      uint8_t* plo = lobuf + ps * 16384;
+      mbar_wait(&bar2[ps], static_cast<uint32_t>((kp / NSLOT) & 1));
       tc::fence_after();
-      tc::gemm3(d1, x, lo, dh_hi, dh_lo);
-      tc::commit(mma_bar);
-    }
-    mbar_wait(mma_bar, mphase);
-    mphase ^= 1;
-    tc::fence_after();
-    uint32_t z[32];
-    tc::ld32(d1 + lane_addr, z);
-    // Z_b^T as the pass-2 A operand: row (b, n), column i   [m = (b, i)]
-    {
-      const uint32_t b = m >> 5, i = m & 31;
+      uint32_t y[16];
+      tc::ld16(tmem + 64 * ps + 32 + c0 + lane_addr, y);
+      const uint32_t b = m >> 5, n = m & 31;  // Y_b[j][n] = D2[(b, n)][j]
 #pragma unroll
-      for (int n = 0; n < 32; ++n) {
-        const float zv = __uint_as_float(z[n]);
+      for (int j = 0; j < 16; ++j)
+        *reinterpret_cast<uint32_t*>(plo + tc::sw(b * 32 + c0 + j, n)) = y[j];
+      fence_proxy_async_smem();
+      tc::fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        const int64_t tp = tile_of(kp);
+        issue_tile_io<float, 32, 32, 4, OUT_MODE>(false, plo, &out_map, nullptr, tp, geom,
+                                                  tile_blocks<4, OUT_MODE>(tp, geom));
+        bulk_commit();
+        // the stage of tile k-2 is free (both its GEMMs have read it): refill S ahead
+        const int64_t kn = kp + S;
+        if (kn < mine) {
+          const int64_t tn = tile_of(kn);
+          const int nb = tile_blocks<4, IN_MODE>(tn, geom);
+          mbar_arrive_expect_tx(&full[kp % S], 4096 * nb);
+          issue_tile_io<float, 32, 32, 4, IN_MODE>(true, stages + (kp % S) * 16384, &in_map,
+                                                   &full[kp % S], tn, geom, nb);
+        }
+      }
+    }
+    // ---- B(k-1): Z^T operand from TMEM, GEMM2(k-1)
+    if (k >= 1 && k - 1 < mine) {
+      const int64_t kb = k - 1;
+      const int bs = static_cast<int>(kb % NSLOT);
+      uint8_t* x = stages + (kb % S) * 16384;
+      uint8_t* lo = lobuf + bs * 16384;
+      mbar_wait(&bar1[bs], static_cast<uint32_t>((kb / NSLOT) & 1));
+      tc::fence_after();
+      uint32_t z[16];
+      tc::ld16(tmem + 64 * bs + c0 + lane_addr, z);
+      const uint32_t b = m >> 5, i = m & 31;  // A2[(b, n)][i] = Z_b[i][n]
+#pragma unroll
+      for (int nn = 0; nn < 16; ++nn) {
+        const float zv = __uint_as_float(z[nn]);
         const uint32_t h = tc::tf32_hi(zv);
-        const uint32_t o = tc::sw(b * 32 + n, i);
+        const uint32_t o = tc::sw(b * 32 + c0 + nn, i);
         *reinterpret_cast<uint32_t*>(x + o) = h;
         *reinterpret_cast<float*>(lo + o) = zv - __uint_as_float(h);
       }
-    }
-    fence_proxy_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      tc::gemm3(d2, x, lo, dv_hi, dv_lo);
-      tc::commit(mma_bar);
-    }
-    mbar_wait(mma_bar, mphase);
-    mphase ^= 1;
-    tc::fence_after();
-    uint32_t y[32];
-    tc::ld32(d2 + lane_addr, y);
-    // Y_b[j][n] = D2[(b, n)][j]   [m = (b, n)]; the output tile reuses `lo`
-    {
-      const uint32_t b = m >> 5, n = m & 31;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) *reinterpret_cast<uint32_t*>(lo + tc::sw(b * 32 + j, n)) = y[j];
-    }
-    fence_proxy_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      issue_tile_io<float, 32, 32, 4, OUT_MODE>(false, lo, &out_map, nullptr, t, geom,
-                                                tile_blocks<4, OUT_MODE>(t, geom));
-      bulk_commit();
-      // stage s is free (both GEMMs have read it): refill it S tiles ahead
-      const int64_t tn = t + static_cast<int64_t>(S) * gridDim.x;
-      if (tn < ntiles) {
-        const int nb = tile_blocks<4, IN_MODE>(tn, geom);
-        mbar_arrive_expect_tx(&full[s], 4096 * nb);
-        issue_tile_io<float, 32, 32, 4, IN_MODE>(true, x, &in_map, &full[s], tn, geom, nb);
+      fence_proxy_async_smem();
+      tc::fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc::fence_after();
+        tc::gemm3(tmem + 64 * bs + 32, x, lo, dv_hi, dv_lo);
+        tc::commit(&bar2[bs]);
       }
-    }
-    if (++s == S) {
-      s = 0;
-      phase ^= 1;
     }
   }
   if (tid == 0) bulk_wait_all();
   tc::fence_before();
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
 }  // namespace dctadj

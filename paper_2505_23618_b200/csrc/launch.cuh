@@ -124,6 +124,9 @@ int launch_tile(const LaunchArgs& a) {
   if (!configured) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) {
       set_last_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
       return ST_ERR_CUDA;
