@@ -144,8 +144,18 @@ int launch_tile(const LaunchArgs& a) {
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * blocks_per_sm;
   const int grid = static_cast<int>(want < cap ? want : cap);
 
-  kern<<<grid, NG * NW * 32, smem, a.stream>>>(in_map, out_map, g, prm);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NG * NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_last_error("tile_kernel launch: %s", cudaGetErrorString(e));
     return ST_ERR_CUDA;

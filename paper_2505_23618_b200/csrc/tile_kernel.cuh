@@ -372,6 +372,11 @@ __global__ void __launch_bounds__(NG * NW * 32)
   // dynamic smem is only guaranteed 16-byte aligned: round up to 1024 for the swizzle atom
   // (pointer arithmetic, not an integer round trip, keeps the shared address space)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // Programmatic dependent launch: this grid may have been scheduled while the
+  // previous kernel in the stream drains; wait for it before touching memory,
+  // and let the next kernel get scheduled as our CTAs retire.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   // `lane`: thread index within the group (0 .. NW*32-1)
   const int grp = threadIdx.x / GT, lane = threadIdx.x % GT;
   uint8_t* ring = smem + grp * S * L::STAGEB;
