@@ -501,24 +501,39 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             fn()
     torch.cuda.synchronize()
 
+    # timed region: K steps back to back, CUDA events only at its two ends (an
+    # event between launches would serialise the kernels' programmatic launch)
     nl = len(w.launches)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(args.steps)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         clk.mark_start()
-        for k in range(args.steps):
-            evs[k][0].record(stream)
-            for j, (_, fn) in enumerate(w.launches):
+        e_start.record(stream)
+        for _ in range(args.steps):
+            for _, fn in w.launches:
                 fn()
-                evs[k][j + 1].record(stream)
+        e_end.record(stream)
         torch.cuda.synchronize()
         clk.mark_end()
         if world > 1:
             dist.barrier()
-    per_launch_ms = [float(np.mean([e[j].elapsed_time(e[j + 1]) for e in evs])) for j in range(nl)]
-    total_ms = evs[0][0].elapsed_time(evs[-1][-1])
+    total_ms = e_start.elapsed_time(e_end)
+    # per-kernel durations (roofline): each launch type back to back on the
+    # same stream, CUDA events around the run
+    per_launch_ms = []
+    reps = max(10, min(args.steps, 200))
+    for _, fn in w.launches:
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        per_launch_ms.append(a.elapsed_time(b) / reps)
 
     e2e_s = None
     if w.e2e is not None:
