@@ -334,14 +334,41 @@ static std::vector<unsigned char> to_dtype(const std::vector<double>& v, int dty
 }
 
 // stream-ordered device copy of a dense matrix; freed with free_dense after use
+// Dense matrices (composites, the exact comparison transforms) are cached on the
+// device by content: a call stream-orders nothing and allocates nothing once the
+// matrix has been seen.  A miss uploads synchronously, so the copy is visible to
+// every stream; entries live until the cache overflows (then the oldest goes,
+// after a device synchronisation inside cudaFree).
+struct DenseCacheEntry {
+  int device, dtype;
+  std::vector<double> m;
+  void* ptr;
+};
+static std::mutex g_dense_mu;
+static std::vector<DenseCacheEntry> g_dense_cache;
+
 static int upload_dense(const AxisPlan& p, int dtype, cudaStream_t st, void** dev) {
+  (void)st;
   *dev = nullptr;
   if (p.dense.empty()) return ST_OK;
+  int device = 0;
+  DA_CUDA(cudaGetDevice(&device));
+  std::lock_guard<std::mutex> lk(g_dense_mu);
+  for (auto& e : g_dense_cache)
+    if (e.device == device && e.dtype == dtype && e.m == p.dense) {
+      *dev = e.ptr;
+      return ST_OK;
+    }
+  if (g_dense_cache.size() >= 64) {
+    DA_CUDA(cudaFree(g_dense_cache.front().ptr));
+    g_dense_cache.erase(g_dense_cache.begin());
+  }
   std::vector<unsigned char> host = to_dtype(p.dense, dtype);
-  const size_t bytes = p.dense.size() * dt_size(dtype);
-  DA_CUDA(cudaMallocAsync(dev, bytes, st));
-  DA_CUDA(cudaMemcpyAsync(*dev, host.data(), bytes, cudaMemcpyHostToDevice, st));
-  // pageable source: the runtime has staged it before returning, so `host` may die
+  void* ptr = nullptr;
+  DA_CUDA(cudaMalloc(&ptr, host.size()));
+  DA_CUDA(cudaMemcpy(ptr, host.data(), host.size(), cudaMemcpyHostToDevice));
+  g_dense_cache.push_back({device, dtype, p.dense, ptr});
+  *dev = ptr;
   return ST_OK;
 }
 
@@ -375,8 +402,7 @@ static int prepare(Launch& L, const AxisPlan& row, const AxisPlan* col, int dtyp
 }
 
 static int finish(Launch& L, cudaStream_t st) {
-  if (L.dense_row) DA_CUDA(cudaFreeAsync(L.dense_row, st));
-  if (L.dense_col) DA_CUDA(cudaFreeAsync(L.dense_col, st));
+  (void)st;  // dense matrices stay in the device cache
   L.dense_row = L.dense_col = nullptr;
   return ST_OK;
 }
@@ -444,11 +470,30 @@ static bool dense_tc_enabled() {
   return v;
 }
 
+// one zeroed [next, done] counter pair per (device, stream): launches on one stream
+// are ordered, and the last CTA of each launch re-zeroes it
+static int stream_sched_counter(cudaStream_t st, unsigned long long** out) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, cudaStream_t>, unsigned long long*>> tab;
+  int device = 0;
+  DA_CUDA(cudaGetDevice(&device));
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : tab)
+    if (e.first.first == device && e.first.second == st) {
+      *out = e.second;
+      return ST_OK;
+    }
+  unsigned long long* p = nullptr;
+  DA_CUDA(cudaMalloc(&p, 2 * sizeof(unsigned long long)));
+  DA_CUDA(cudaMemset(p, 0, 2 * sizeof(unsigned long long)));
+  tab.push_back({{device, st}, p});
+  *out = p;
+  return ST_OK;
+}
+
 template <int IN_MODE, int OUT_MODE>
 static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, int tiles_x) {
-  // a stage is held from the tile's load until both GEMMs have read it (3 pipeline
-  // phases): S = 8 leaves 5 tiles (80 KB) of loads in flight per SM
-  constexpr int S = 8;
+  constexpr int S = 8;  // ring of 8 x 16 KB + 4 group tiles x 16 KB: 208 KB, one CTA/SM
   Geom g{};
   g.nblocks = nblocks;
   g.ntiles = (nblocks + 3) / 4;
@@ -457,27 +502,79 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   LaunchArgs la = a;
   la.rows = nblocks * 32;
   CUtensorMap in_map, out_map;
-  int rc = make_map<float, 32, 32, 4, IN_MODE>(&in_map, a.in, la);
-  if (!rc) rc = make_map<float, 32, 32, 4, OUT_MODE>(&out_map, a.out, la);
+  auto map_for = [&](CUtensorMap* m, const void* base, int mode) {
+    if (mode == MODE_FRAME4) {  // {col in block, block column, frame row, frame}
+      uint64_t dims[4] = {32, static_cast<uint64_t>(tiles_x), static_cast<uint64_t>(a.frame_h),
+                          static_cast<uint64_t>(a.frames)};
+      uint64_t strides[3] = {128, static_cast<uint64_t>(a.frame_w) * 4,
+                             static_cast<uint64_t>(a.frame_w) * a.frame_h * 4};
+      uint32_t box[4] = {32, 4, 32, 1};
+      return encode_tensor_map(m, DT_F32, 4, dims, strides, box, 128, const_cast<void*>(base));
+    }
+    return mode == MODE_FRAME ? make_map<float, 32, 32, 4, MODE_FRAME>(m, base, la)
+                              : make_map<float, 32, 32, 4, MODE_LINEAR>(m, base, la);
+  };
+  int rc = map_for(&in_map, a.in, IN_MODE);
+  if (!rc) rc = map_for(&out_map, a.out, OUT_MODE);
   if (rc) return rc;
-  DenseTcParams prm{static_cast<const float*>(a.dense_row), static_cast<const float*>(a.dense_col)};
+  DenseTcParams prm{static_cast<const float*>(a.dense_row), static_cast<const float*>(a.dense_col),
+                    nullptr, nullptr};
+  int rc_s = stream_sched_counter(a.stream, &prm.sched);
+  if (rc_s) return rc_s;
+  // diagnostics: DCTADJ_TC_TRACE=<file> dumps CTA 0's per-tile event clocks
+  static const char* trace_file = std::getenv("DCTADJ_TC_TRACE");
+  const size_t trace_bytes =
+      sizeof(unsigned long long) * (kTcTraceTiles * kTcTraceEv + 2 * kTcTraceCtas);
+  if (trace_file) {
+    DA_CUDA(cudaMalloc(&prm.trace, trace_bytes));
+    DA_CUDA(cudaMemsetAsync(prm.trace, 0, trace_bytes, a.stream));
+  }
   auto kern = dense_tc_kernel<S, IN_MODE, OUT_MODE>;
-  const size_t smem = 1024 + S * 16384 + 3 * 16384 + 16384 + (S + 6) * 8 + 16;
+  const size_t smem =
+      1024 + S * 16384 + kDenseTcGroups * 16384 + 16384 + (2 * S + 4 * kDenseTcGroups) * 8 +
+      (S + 1) * 8 + 16;
   static int bps = 0;
   if (!bps) {
     DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
-    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, smem));
+    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kDenseTcThreads, smem));
     if (bps < 1) return fail(ST_ERR_CUDA, "dense tensor-core kernel does not fit an SM");
-    bps = std::min(bps, 2);  // 256 TMEM columns per CTA, 512 per SM
+    bps = std::min(bps, 512 / (128 * kDenseTcGroups));  // TMEM columns per SM
     if (trace_on())
       std::fprintf(stderr, "[dctadj] dense_tc: %zu B smem, %d CTAs/SM\n", smem, bps);
   }
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * bps;
-  kern<<<static_cast<int>(std::min<int64_t>(g.ntiles, cap)), 256, smem, a.stream>>>(in_map, out_map,
-                                                                                    g, prm);
-  DA_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(g.ntiles, cap)));
+  cfg.blockDim = dim3(kDenseTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm));
+  if (trace_file) {
+    std::vector<unsigned long long> h(kTcTraceTiles * kTcTraceEv + 2 * kTcTraceCtas);
+    DA_CUDA(cudaMemcpyAsync(h.data(), prm.trace, trace_bytes, cudaMemcpyDeviceToHost, a.stream));
+    DA_CUDA(cudaStreamSynchronize(a.stream));
+    DA_CUDA(cudaFree(prm.trace));
+    if (FILE* f = std::fopen(trace_file, "w")) {
+      for (int k = 0; k < kTcTraceTiles; ++k) {
+        for (int e = 0; e < kTcTraceEv; ++e) std::fprintf(f, "%llu ", h[k * kTcTraceEv + e]);
+        std::fprintf(f, "\n");
+      }
+      // per-CTA start / end globaltimer (ns), 8 per line
+      for (int c = 0; c < kTcTraceCtas; ++c) {
+        for (int e = 0; e < 8; ++e)
+          std::fprintf(f, "%llu ", e < 2 ? h[kTcTraceTiles * kTcTraceEv + 2 * c + e] : 0ull);
+        std::fprintf(f, "\n");
+      }
+      std::fclose(f);
+    }
+  }
   return ST_OK;
 }
 
@@ -512,12 +609,15 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
     a.dense_col = L.dense_col;
     a.stream = st;
     const int ty = (fh + H - 1) / H, tx = fw / W;
+    const bool f4 = tx % 4 == 0;  // super-tiles never straddle a block row
     if (in_mode == MODE_LINEAR && out_mode == MODE_LINEAR)
       rc = launch_dense_tc<MODE_LINEAR, MODE_LINEAR>(a, nblk, 0, 0);
     else if (in_mode == MODE_FRAME)
-      rc = launch_dense_tc<MODE_FRAME, MODE_LINEAR>(a, nblk, ty, tx);
+      rc = f4 ? launch_dense_tc<MODE_FRAME4, MODE_LINEAR>(a, nblk, ty, tx)
+              : launch_dense_tc<MODE_FRAME, MODE_LINEAR>(a, nblk, ty, tx);
     else
-      rc = launch_dense_tc<MODE_LINEAR, MODE_FRAME>(a, nblk, ty, tx);
+      rc = f4 ? launch_dense_tc<MODE_LINEAR, MODE_FRAME4>(a, nblk, ty, tx)
+              : launch_dense_tc<MODE_LINEAR, MODE_FRAME>(a, nblk, ty, tx);
     int rc2 = finish(L, st);
     return rc ? rc : rc2;
   }
@@ -950,7 +1050,6 @@ int dctadj_dense(const double* m, int32_t rows, const void* x, void* y, int64_t 
                                                      static_cast<const double*>(x),
                                                      static_cast<double*>(y), nvec, n);
   DA_CUDA(cudaGetLastError());
-  DA_CUDA(cudaFreeAsync(dm, st));
   return ST_OK;
 }
 

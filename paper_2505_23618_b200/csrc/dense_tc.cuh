@@ -5,15 +5,18 @@
 // two tcgen05.mma (kind::tf32) GEMMs per super-tile of 4 blocks, in 3xTF32
 // (a = a_hi + a_lo; a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi: fp32-level error).
 //
-//   pass 1  D1[(b,i)][n] = sum_k X_b[i][k] Dh[n][k]        M=128 (4 blocks x 32 rows), N=32, K=32
-//   pass 2  D2[(b,n)][j] = sum_i Z_b[i][n] Dv[j][i]         (Z_b^T as the A operand)
-//   Y_b[j][n] = D2[(b,n)][j]
+//   pass 1  D1[(b,j)][r] = sum_i X_b[i][j] Dv[r][i]     M=128 (4 blocks x 32), N=32, K=32
+//   pass 2  D2[(b,r)][n] = sum_j W_b[r][j] Dh[n][j]     W_b = Dv X_b;  Y_b[r][n] = D2[(b,r)][n]
 //
-// Operands are K-major 128-byte-swizzled smem tiles: the TMA-loaded block tile
-// (P=4 blocks = 128 rows x 128 B) IS the pass-1 A operand.  Accumulators live
-// in TMEM (2 x 32 columns); each of the 128 threads owns one TMEM lane and
-// moves its row with tcgen05.ld, writing the transposed operand / output tile.
-// One elected thread issues the MMAs; completion is tcgen05.commit -> mbarrier.
+// The data operand (A) lives in TENSOR MEMORY, not shared memory: the kernel is
+// bound by shared-memory bandwidth once HBM is streamed, and an smem A operand
+// is re-read by every MMA of the 3xTF32 split.  Each epilogue thread owns one
+// TMEM lane: it reads its column of the TMA-loaded block (conflict-free on the
+// 128-byte swizzle), splits it into tf32 hi / lo and tcgen05.st's both into the
+// A columns; after pass 1 it transposes W through a per-warp 4 KB smem tile and
+// stores the pass-2 A operand the same way.  Only the 32x32 coefficient
+// matrices (hi / lo, 16 KB) are smem (B) operands.  One elected thread issues
+// the MMAs; completion is tcgen05.commit -> mbarrier.
 #pragma once
 #include "tile_kernel.cuh"
 
@@ -101,42 +104,132 @@ DA_DEV void gemm3(uint32_t tmem_d, const uint8_t* ahi, const uint8_t* alo, const
 struct DenseTcParams {
   const float* dh;  // device 32x32: row-pass matrix (Y = Dv X Dh^T)
   const float* dv;  // device 32x32: column-pass matrix
+  unsigned long long* trace;  // diagnostics (DCTADJ_TC_TRACE): CTA 0 event clocks, or null
+  unsigned long long* sched;  // [next, done]: dynamic tile counter, zero between launches
 };
+constexpr int kTcTraceTiles = 128, kTcTraceEv = 8, kTcTraceCtas = 1024;
+DA_DEV unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
-// S-stage TMA ring of 4-block super-tiles; one CTA = 8 warps: warps w and w+4
-// share TMEM lane quadrant w%4 (tile rows 32(w%4) ..), each moving 16 of the 32
-// columns.
-// Three tiles are in flight per CTA (TMEM and `lo` buffers triple-buffered) so
-// each tensor-core GEMM hides behind a full phase of thread work:
-//   iteration k:  A(k)   split X_k into tf32 hi / lo, issue GEMM1(k)
-//                 C(k-2) wait GEMM2(k-2), TMEM -> Y tile, TMA store, refill
-//                 B(k-1) wait GEMM1(k-1), TMEM -> Z^T operand, issue GEMM2(k-1)
+constexpr int kDenseTcGroups = 4;
+constexpr int kDenseTcThreads = (4 * kDenseTcGroups + 3) * 32;
+
+namespace tc {
+// D (+)= A_hi B_hi + A_hi B_lo + A_lo B_hi over K = 32, A in TMEM (hi at
+// columns a..a+31, lo at a+32..a+63; one tf32 per column, lane = row)
+DA_DEV void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, bool accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(static_cast<uint32_t>(accumulate)), "r"(kIdesc)
+      : "memory");
+}
+DA_DEV void gemm3_ts(uint32_t tmem_d, uint32_t tmem_a, const uint8_t* bhi, const uint8_t* blo) {
+  const uint64_t dbh = desc_k_sw128(bhi), dbl = desc_k_sw128(blo);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint64_t off = static_cast<uint64_t>(k * 32) >> 4;  // 8 tf32 = 32 bytes along K
+    mma_tf32_ts(tmem_d, tmem_a + 8 * k, dbh + off, k > 0);
+    mma_tf32_ts(tmem_d, tmem_a + 8 * k, dbl + off, true);
+    mma_tf32_ts(tmem_d, tmem_a + 32 + 8 * k, dbh + off, true);
+  }
+}
+DA_DEV void st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+DA_DEV void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// split v into tf32 hi / lo and store both into this thread's TMEM lane
+DA_DEV void st_split(uint32_t taddr, uint32_t (&v)[32]) {
+  uint32_t lo[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const uint32_t h = tf32_hi(__uint_as_float(v[c]));
+    lo[c] = __float_as_uint(__uint_as_float(v[c]) - __uint_as_float(h));
+    v[c] = h;
+  }
+  st32(taddr, v);
+  st32(taddr + 32, lo);
+}
+}  // namespace tc
+
+// super-tile t of the LINEAR / FRAME / FRAME4 side (4 blocks of 32 x 32 fp32)
+template <int MODE>
+DA_DEV void tc_tile_io(bool load, uint8_t* buf, const CUtensorMap* map, uint64_t* bar, int64_t t,
+                       const Geom& g) {
+  if constexpr (MODE == MODE_FRAME4) {
+    const int64_t per = static_cast<int64_t>(g.tiles_x) * g.tiles_y, blk = 4 * t;
+    const int f = static_cast<int>(blk / per);
+    const int rem = static_cast<int>(blk - f * per);
+    const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+    if (load)
+      tma_load_4d(buf, map, bar, 0, tx, ty * 32, f);
+    else
+      tma_store_4d(map, buf, 0, tx, ty * 32, f);
+  } else {
+    issue_tile_io<float, 32, 32, 4, MODE>(load, buf, map, bar, t, g, tile_blocks<4, MODE>(t, g));
+  }
+}
+// smem tile row of (block b, block row r)
+template <int MODE>
+DA_DEV uint32_t tc_row(uint32_t b, uint32_t r) {
+  return MODE == MODE_FRAME4 ? r * 4 + b : b * 32 + r;
+}
+
+// Warp-specialised pipeline (one CTA per SM, 4 * NGRP + 3 warps):
+//   warp 4*NGRP     TMA producer: S-stage ring of 4-block super-tiles (16 KB)
+//   warps 4*NGRP+1, +2  MMA issuers (one lane each) for pass 1 / pass 2, in tile
+//                   order, as soon as the owning group signals (two issuers: a
+//                   single thread issuing 24 small MMAs per tile is the pace)
+//   warps 0..4*NGRP-1  NGRP epilogue groups of 4 warps; group g handles tiles
+//                   k = g (mod NGRP); warp w owns TMEM lane quadrant w % 4 (= block
+//                   b of the super-tile), so a group covers all 128 lanes of its
+//                   TMEM slot: A (hi, lo: 64 columns), D1 (32), D2 (32)
+// Hand-offs are mbarriers: full/empty (ring), a1_ready / d1_done / a2_ready /
+// d2_done per group; a group's threads meet at a named barrier before its
+// elected thread arrives or issues the TMA store of Y (staged in the group's
+// 16 KB smem tile, which also carries the per-warp W transposes).
 template <int S, int IN_MODE, int OUT_MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kDenseTcThreads, 1)
     dense_tc_kernel(const __grid_constant__ CUtensorMap in_map,
                     const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
                     const __grid_constant__ DenseTcParams prm) {
+  constexpr int NGRP = kDenseTcGroups;
+  static_assert(NGRP * 128 <= 512, "TMEM columns");
   using L = TileLayout<float, 32, 32, 4>;  // 128 rows x 128 B, SW128
   static_assert(L::TILEB == 16384 && L::STAGEB == 16384, "4 blocks of 32x32 fp32");
-  static_assert(S >= 4, "a stage is held from A(k) until C(k)");
-  constexpr int NSLOT = 3;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* stages = smem;                       // S x 16 KB: X tile, then Z^T hi
-  uint8_t* lobuf = smem + S * 16384;            // NSLOT x 16 KB: X lo, then Z^T lo, then Y
-  uint8_t* bmat = lobuf + NSLOT * 16384;        // 4 x 4 KB: Dh hi/lo, Dv hi/lo (32 rows)
-  uint8_t* dh_hi = bmat;
-  uint8_t* dh_lo = bmat + 4096;
-  uint8_t* dv_hi = bmat + 8192;
-  uint8_t* dv_lo = bmat + 12288;
+  uint8_t* stages = smem;                     // S x 16 KB: X tiles as loaded
+  uint8_t* gtile = smem + S * 16384;          // NGRP x 16 KB: W transpose / Y staging
+  uint8_t* bmat = gtile + NGRP * 16384;       // 4 x 4 KB: Dv hi/lo, Dh hi/lo (32 rows)
+  uint8_t* dv_hi = bmat;
+  uint8_t* dv_lo = bmat + 4096;
+  uint8_t* dh_hi = bmat + 8192;
+  uint8_t* dh_lo = bmat + 12288;
   uint64_t* full = reinterpret_cast<uint64_t*>(bmat + 16384);
-  uint64_t* bar1 = full + S;       // GEMM1 done, per slot
-  uint64_t* bar2 = bar1 + NSLOT;   // GEMM2 done, per slot
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar2 + NSLOT);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  uint64_t* empty = full + S;
+  uint64_t* a1_ready = empty + S;  // per group
+  uint64_t* d1_done = a1_ready + NGRP;
+  uint64_t* a2_ready = d1_done + NGRP;
+  uint64_t* d2_done = a2_ready + NGRP;
+  int64_t* tile_id = reinterpret_cast<int64_t*>(d2_done + NGRP);  // per ring stage; -1 = end
+  volatile int64_t* total_k = tile_id + S;  // tiles this CTA got (-1 until known)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_id + S + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // constant operands: split Dh, Dv into tf32 hi / lo, K-major SW128 (32 rows)
-  for (int e = tid; e < 1024; e += 256) {
+  // constant B operands: Dv, Dh split into tf32 hi / lo, K-major SW128 (32 rows)
+  for (int e = tid; e < 1024; e += kDenseTcThreads) {
     const int r = e >> 5, c = e & 31;
     const float h = prm.dh[e], v = prm.dv[e];
     const uint32_t hh = tc::tf32_hi(h), vh = tc::tf32_hi(v);
@@ -146,16 +239,23 @@ __global__ void __launch_bounds__(256)
     *reinterpret_cast<float*>(dv_lo + tc::sw(r, c)) = v - __uint_as_float(vh);
   }
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
-    for (int j = 0; j < NSLOT; ++j) {
-      mbar_init(&bar1[j], 1);
-      mbar_init(&bar2[j], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
     }
+    for (int g = 0; g < NGRP; ++g) {
+      mbar_init(&a1_ready[g], 1);
+      mbar_init(&d1_done[g], 1);
+      mbar_init(&a2_ready[g], 1);
+      mbar_init(&d2_done[g], 1);
+    }
+    *total_k = -1;
     fence_mbar_init();
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                     smem_u32(tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(128 * NGRP)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -164,119 +264,164 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t quad = warp & 3, half = warp >> 2;
-  const uint32_t lane_addr = (quad * 32) << 16;
-  const uint32_t m = quad * 32 + (tid & 31);  // TMEM lane / tile row owned by this thread
-  const uint32_t c0 = half * 16;              // the 16 columns this thread moves
+  if (prm.trace && tid == 0 && blockIdx.x < kTcTraceCtas)
+    prm.trace[kTcTraceTiles * kTcTraceEv + 2 * blockIdx.x] = globaltimer();
 
+  // everything above overlaps the previous kernel's tail (programmatic launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t ntiles = geom.ntiles;
-  const int64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  auto tile_of = [&](int64_t k) { return blockIdx.x + k * gridDim.x; };
-  if (tid == 0) {
-    for (int s = 0; s < S && s < mine; ++s) {
-      const int64_t t = tile_of(s);
-      const int nb = tile_blocks<4, IN_MODE>(t, geom);
-      mbar_arrive_expect_tx(&full[s], 4096 * nb);
-      issue_tile_io<float, 32, 32, 4, IN_MODE>(true, stages + s * 16384, &in_map, &full[s], t,
-                                               geom, nb);
-    }
-  }
 
-  for (int64_t k = 0; k < mine + 2; ++k) {
-    // ---- A(k): split X_k into tf32 hi (in place) and lo; GEMM1(k)
-    if (k < mine) {
-      const int slot = static_cast<int>(k % NSLOT);
-      uint8_t* x = stages + (k % S) * 16384;
-      uint8_t* lo = lobuf + slot * 16384;
-      mbar_wait(&full[k % S], static_cast<uint32_t>((k / S) & 1));
-      if (tid == 0) bulk_wait_read<0>();  // Y(k-3), stored from this lo buffer, is read
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t o = tc::sw(m, c0 + q * 4);
-        const float4 v = *reinterpret_cast<const float4*>(x + o);
-        const uint4 h =
-            make_uint4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
-        *reinterpret_cast<uint4*>(x + o) = h;
-        *reinterpret_cast<float4*>(lo + o) =
-            make_float4(v.x - __uint_as_float(h.x), v.y - __uint_as_float(h.y),
-                        v.z - __uint_as_float(h.z), v.w - __uint_as_float(h.w));
-      }
-      fence_proxy_async_smem();
-      tc::fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after();
-        tc::gemm3(tmem + 64 * slot, x, lo, dh_hi, dh_lo);
-        tc::commit(&bar1[slot]);
-      }
-    }
-    // ---- C(k-2): Y(k-2) from TMEM, store, refill its stage
-    if (k >= 2 && k - 2 < mine) {
-      const int64_t kp = k - 2;
-      const int ps = static_cast<int>(kp % NSLOT);
-      uint8_t* plo = lobuf + ps * 16384;
-      mbar_wait(&bar2[ps], static_cast<uint32_t>((kp / NSLOT) & 1));
-      tc::fence_after();
-      uint32_t y[16];
-      tc::ld16(tmem + 64 * ps + 32 + c0 + lane_addr, y);
-      const uint32_t b = m >> 5, n = m & 31;  // Y_b[j][n] = D2[(b, n)][j]
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        *reinterpret_cast<uint32_t*>(plo + tc::sw(b * 32 + c0 + j, n)) = y[j];
-      fence_proxy_async_smem();
-      tc::fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        const int64_t tp = tile_of(kp);
-        issue_tile_io<float, 32, 32, 4, OUT_MODE>(false, plo, &out_map, nullptr, tp, geom,
-                                                  tile_blocks<4, OUT_MODE>(tp, geom));
-        bulk_commit();
-        // the stage of tile k-2 is free (both its GEMMs have read it): refill S ahead
-        const int64_t kn = kp + S;
-        if (kn < mine) {
-          const int64_t tn = tile_of(kn);
-          const int nb = tile_blocks<4, IN_MODE>(tn, geom);
-          mbar_arrive_expect_tx(&full[kp % S], 4096 * nb);
-          issue_tile_io<float, 32, 32, 4, IN_MODE>(true, stages + (kp % S) * 16384, &in_map,
-                                                   &full[kp % S], tn, geom, nb);
+  if (warp == 4 * NGRP) {
+    // ---------------- TMA producer; chunks of CH tiles: blockIdx.x, then from a
+    // global counter, the next chunk's atomic in flight while this one loads
+    if (lane == 0) {
+      constexpr int CH = 4;
+      int64_t k = 0;
+      int64_t chunk = blockIdx.x;
+      unsigned long long nxt = atomicAdd(prm.sched, 1ull);
+      for (;;) {
+        const int64_t t0 = chunk * CH;
+        if (t0 >= ntiles) break;
+        for (int64_t t = t0; t < t0 + CH && t < ntiles; ++t, ++k) {
+          const int s = static_cast<int>(k % S);
+          mbar_wait(&empty[s], static_cast<uint32_t>(((k / S) & 1) ^ 1));
+          tile_id[s] = t;
+          const int nb = IN_MODE == MODE_FRAME4 ? 4 : tile_blocks<4, IN_MODE>(t, geom);
+          mbar_arrive_expect_tx(&full[s], 4096 * nb);
+          tc_tile_io<IN_MODE>(true, stages + s * 16384, &in_map, &full[s], t, geom);
         }
+        chunk = gridDim.x + static_cast<int64_t>(nxt);
+        if (chunk * CH < ntiles) nxt = atomicAdd(prm.sched, 1ull);
+      }
+      *total_k = k;
+      asm volatile("griddepcontrol.launch_dependents;" :::);
+      for (int j = 0; j < NGRP; ++j, ++k) {  // one end marker per epilogue group
+        const int s = static_cast<int>(k % S);
+        mbar_wait(&empty[s], static_cast<uint32_t>(((k / S) & 1) ^ 1));
+        tile_id[s] = -1;
+        mbar_arrive(&full[s]);
       }
     }
-    // ---- B(k-1): Z^T operand from TMEM, GEMM2(k-1)
-    if (k >= 1 && k - 1 < mine) {
-      const int64_t kb = k - 1;
-      const int bs = static_cast<int>(kb % NSLOT);
-      uint8_t* x = stages + (kb % S) * 16384;
-      uint8_t* lo = lobuf + bs * 16384;
-      mbar_wait(&bar1[bs], static_cast<uint32_t>((kb / NSLOT) & 1));
-      tc::fence_after();
-      uint32_t z[16];
-      tc::ld16(tmem + 64 * bs + c0 + lane_addr, z);
-      const uint32_t b = m >> 5, i = m & 31;  // A2[(b, n)][i] = Z_b[i][n]
-#pragma unroll
-      for (int nn = 0; nn < 16; ++nn) {
-        const float zv = __uint_as_float(z[nn]);
-        const uint32_t h = tc::tf32_hi(zv);
-        const uint32_t o = tc::sw(b * 32 + c0 + nn, i);
-        *reinterpret_cast<uint32_t*>(x + o) = h;
-        *reinterpret_cast<float*>(lo + o) = zv - __uint_as_float(h);
+  } else if (warp == 4 * NGRP + 1 || warp == 4 * NGRP + 2) {
+    // ---------------- MMA issuers: pass 1 / pass 2, each in tile order
+    const bool pass1 = warp == 4 * NGRP + 1;
+    uint64_t* ready = pass1 ? a1_ready : a2_ready;
+    uint64_t* done = pass1 ? d1_done : d2_done;
+    const uint8_t* bhi = pass1 ? dv_hi : dh_hi;
+    const uint8_t* blo = pass1 ? dv_lo : dh_lo;
+    const uint32_t dcol = pass1 ? 64 : 96;
+    if (lane == 0) {
+      for (int64_t k = 0;; ++k) {
+        const int g = static_cast<int>(k % NGRP);
+        const uint32_t par = static_cast<uint32_t>((k / NGRP) & 1);
+        bool ok;
+        while (!(ok = mbar_test(&ready[g], par))) {
+          const int64_t tot = *total_k;
+          if (tot >= 0 && k >= tot) break;
+        }
+        if (!ok) break;
+        if (pass1 && prm.trace && blockIdx.x == 0 && k < kTcTraceTiles)
+          prm.trace[k * kTcTraceEv + 7] = clock64();
+        tc::fence_after();
+        tc::gemm3_ts(tmem + 128 * g + dcol, tmem + 128 * g, bhi, blo);
+        tc::commit(&done[g]);
       }
+    }
+  } else {
+    // ---------------- epilogue groups
+    const int g = warp >> 2;
+    const uint32_t b = warp & 3;  // block of the super-tile = TMEM lane quadrant
+    const uint32_t lane_addr = (b * 32) << 16;
+    const bool leader = b == 0 && lane == 0;
+    uint8_t* gt = gtile + g * 16384;
+    const uint32_t ta = tmem + 128 * g + lane_addr;  // this lane's A / D1 / D2 columns
+    auto group_bar = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); };
+    const bool tr = prm.trace && blockIdx.x == 0 && leader;
+    auto ev = [&](int64_t k, int e) {
+      if (tr && k < kTcTraceTiles) prm.trace[k * kTcTraceEv + e] = clock64();
+    };
+    for (int64_t k = g;; k += NGRP) {
+      const int s = static_cast<int>(k % S);
+      const uint32_t gp = static_cast<uint32_t>((k / NGRP) & 1);  // this group's use parity
+      const uint8_t* x = stages + s * 16384;
+      uint32_t v[32];
+      // pass-1 A: column j = lane of block b, A[(b,j)][i] = X_b[i][j]
+      ev(k, 0);
+      mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
+      const int64_t t = tile_id[s];
+      if (t < 0) break;
+      ev(k, 1);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        v[i] = *reinterpret_cast<const uint32_t*>(x + tc::sw(tc_row<IN_MODE>(b, i), lane));
+      tc::st_split(ta, v);
+      tc::wait_st();
+      if (leader) bulk_wait_read<0>();  // Y(k - NGRP) has left the group tile
+      tc::fence_before();
+      group_bar();
+      if (leader) {
+        mbar_arrive(&empty[s]);
+        mbar_arrive(&a1_ready[g]);
+      }
+      ev(k, 2);
+      // W_b = Dv X_b: lane j holds column j; transpose through this warp's 4 KB
+      mbar_wait(&d1_done[g], gp);
+      tc::fence_after();
+      ev(k, 3);
+      tc::ld32(ta + 64, v);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) *reinterpret_cast<uint32_t*>(gt + tc::sw(b * 32 + r, lane)) = v[r];
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 w = *reinterpret_cast<const uint4*>(gt + tc::sw(b * 32 + lane, q * 4));
+        v[4 * q] = w.x;
+        v[4 * q + 1] = w.y;
+        v[4 * q + 2] = w.z;
+        v[4 * q + 3] = w.w;
+      }
+      tc::st_split(ta, v);  // pass-2 A: row r = lane, A[(b,r)][j] = W_b[r][j]
+      tc::wait_st();
+      tc::fence_before();
+      group_bar();
+      if (leader) mbar_arrive(&a2_ready[g]);
+      ev(k, 4);
+      // Y_b rows from TMEM into the group tile, TMA store
+      mbar_wait(&d2_done[g], gp);
+      tc::fence_after();
+      ev(k, 5);
+      tc::ld32(ta + 96, v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<uint4*>(gt + tc::sw(tc_row<OUT_MODE>(b, lane), q * 4)) =
+            make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       fence_proxy_async_smem();
       tc::fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after();
-        tc::gemm3(tmem + 64 * bs + 32, x, lo, dv_hi, dv_lo);
-        tc::commit(&bar2[bs]);
+      group_bar();
+      if (leader) {
+        tc_tile_io<OUT_MODE>(false, gt, &out_map, nullptr, t, geom);
+        bulk_commit();
       }
+      ev(k, 6);
     }
+    if (leader) bulk_wait_all();
   }
-  if (tid == 0) bulk_wait_all();
   tc::fence_before();
   __syncthreads();
+  if (prm.trace && tid == 0 && blockIdx.x < kTcTraceCtas)
+    prm.trace[kTcTraceTiles * kTcTraceEv + 2 * blockIdx.x + 1] = globaltimer();
+  if (tid == 0) {  // the last CTA out re-arms the tile counter for the next launch
+    __threadfence();
+    if (atomicAdd(prm.sched + 1, 1ull) == gridDim.x - 1) {
+      prm.sched[0] = 0;
+      prm.sched[1] = 0;
+      __threadfence();
+    }
+  }
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(128 * NGRP)
+                 : "memory");
 }
 
 }  // namespace dctadj

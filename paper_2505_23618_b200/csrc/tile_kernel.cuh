@@ -42,6 +42,19 @@ DA_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+DA_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+DA_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 DA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -71,6 +84,21 @@ DA_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1
                    map),
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
+}
+DA_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                        int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+DA_DEV void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
 }
 DA_DEV void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
   asm volatile(
@@ -143,7 +171,11 @@ struct TileLayout {
 // FRAME:  blocks in raster order of (F, height, width) frames.
 // GATHER: block i of a class list sits at element offset offsets[i] of a packed
 //         mixed-shape buffer viewed as [elements / W, W] (config 3).
-enum Mode : int { MODE_LINEAR = 0, MODE_FRAME = 1, MODE_GATHER = 2 };
+// MODE_FRAME4 (tensor-core dense kernel only): a super-tile of 4 horizontally
+// adjacent blocks moves as ONE 4-D box {32 cols, 4 blocks, 32 rows, 1 frame}, so
+// each frame row is a single 512-byte segment; the smem tile is then row-
+// interleaved (tile row = 4 * block row + block) instead of block-major.
+enum Mode : int { MODE_LINEAR = 0, MODE_FRAME = 1, MODE_GATHER = 2, MODE_FRAME4 = 3 };
 
 struct Geom {
   int64_t ntiles;      // super-tiles

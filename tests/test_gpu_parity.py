@@ -427,3 +427,59 @@ def test_encoder_eval_errors_and_numpy_block():
         pipeline.simultaneous_encoder_eval(np.zeros((64, 64)), pipeline.EncoderContext(s32, s32))
     out = pipeline.simultaneous_encoder_eval(np.zeros((32, 32)), pipeline.EncoderContext(s32, s32))
     assert len(out) == 5 and all(np.array_equal(v, np.zeros((32, 32))) for v in out.values())
+
+
+# ------------------------------------------- dense 32x32 fp32 on the tensor cores
+# (csrc/dense_tc.cuh: 3xTF32 tcgen05 kernel, TMEM operands, dynamic tile counter)
+def _dense_pair(seed_h, seed_v):
+    mk = lambda s: pipeline.make_adjusted_transform(  # noqa: E731
+        random_adjustment(SparsityPattern.dense(32), Side.POST, TransformKind.DCT2, s))
+    return mk(seed_h), mk(seed_v)
+
+
+@pytest.mark.parametrize("nblk", [1, 3, 4, 5, 37, 600, 4099])
+def test_dense_tc_2d_ragged(nblk):
+    """Row and column matrices differ (catches a transposed pass); block counts
+    that are not multiples of the 4-block super-tile; oracle parity both ways."""
+    th, tv = _dense_pair(11, 12)
+    x = np.random.default_rng(nblk).standard_normal((nblk, 32, 32))
+    ah, av = oaxis(th.adjustment), oaxis(tv.adjustment)
+    y = pipeline.forward_adjusted_2d(th, tv, dev(x)).cpu().numpy()
+    assert rel_err(y, O.adjusted_2d(ah, av, x)) < F32_TOL
+    xr = pipeline.inverse_adjusted_2d(th, tv, dev(y)).cpu().numpy()
+    assert rel_err(xr, O.adjusted_2d(ah, av, y.astype(np.float64), inverse=True)) < F32_TOL
+
+
+def test_dense_tc_repeat_and_streams():
+    """The dynamic tile counter re-arms itself: repeated launches on one stream and
+    launches on a second stream give identical results."""
+    th, tv = _dense_pair(13, 14)
+    x = torch.randn(20000, 32, 32, device="cuda")
+    y0 = pipeline.forward_adjusted_2d(th, tv, x)
+    for _ in range(3):
+        assert torch.equal(pipeline.forward_adjusted_2d(th, tv, x), y0)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        y1 = pipeline.forward_adjusted_2d(th, tv, x)
+    s.synchronize()
+    assert torch.equal(y1, y0)
+
+
+@pytest.mark.parametrize("shape", [(2, 70, 256), (1, 32, 128), (3, 33, 384)])
+def test_dense_tc_frames_4wide(shape):
+    """Frames whose width holds a multiple of 4 blocks take the one-box-per-
+    super-tile TMA path (FRAME4): forward against numpy on zero-padded tiles,
+    inverse back to the (clipped) frames."""
+    th, tv = _dense_pair(15, 16)
+    f, h, w = shape
+    fr = np.random.default_rng(h).standard_normal(shape)
+    ty, tx = -(-h // 32), w // 32
+    pad = np.zeros((f, ty * 32, w))
+    pad[:, :h] = fr
+    blocks = pad.reshape(f, ty, 32, tx, 32).transpose(0, 1, 3, 2, 4).reshape(-1, 32, 32)
+    mh, mv = pipeline.dense_matrix(th), pipeline.dense_matrix(tv)
+    want = mv @ blocks @ mh.T
+    y = pipeline.forward_frames(th, tv, dev(fr))
+    assert rel_err(y.cpu().numpy(), want) < F32_TOL
+    back = pipeline.inverse_frames(th, tv, y, h, w).cpu().numpy()
+    assert rel_err(back.reshape(f, h, w), fr) < F32_TOL

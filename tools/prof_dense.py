@@ -22,3 +22,11 @@ for _ in range(iters):
 e1.record()
 torch.cuda.synchronize()
 print(f"dense fwd {e0.elapsed_time(e1) / iters * 1e3:.1f} us per launch")
+import time  # noqa: E402
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(iters):
+    y = pipeline.forward_adjusted_2d(td, td, x)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"host enqueue {(t1 - t0) / iters * 1e6:.1f} us per call")

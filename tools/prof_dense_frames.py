@@ -1,0 +1,23 @@
+"""Dense 32x32 fp32 2-D transform over config-5 frames (64 x 2160 x 3840), the
+tensor-core path; a few back-to-back launches (for ncu / timing)."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2505_23618_b200 import benchmark, pipeline  # noqa: E402
+from paper_2505_23618_b200.transforms import TransformKind, build_transform  # noqa: E402
+
+td = benchmark._dense_transform(build_transform(TransformKind.DST7, 32).entries)
+x = torch.randn(64, 2160, 3840, device="cuda")
+iters = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+y = pipeline.forward_frames(td, td, x)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(iters):
+    y = pipeline.forward_frames(td, td, x)
+e1.record()
+torch.cuda.synchronize()
+print(f"dense frames fwd {e0.elapsed_time(e1) / iters * 1e3:.1f} us per launch")
