@@ -621,6 +621,26 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
     int rc2 = finish(L, st);
     return rc ? rc : rc2;
   }
+  if (in_mode == MODE_FRAME || out_mode == MODE_FRAME) {
+    // frames: the interleaved one-box-per-super-tile kernel when the frame width
+    // holds whole super-tiles (it declines otherwise), else the per-block boxes
+    const int il_in = in_mode == MODE_FRAME ? MODE_FRAME_IL : MODE_LINEAR_IL;
+    const int il_out = out_mode == MODE_FRAME ? MODE_FRAME_IL : MODE_LINEAR_IL;
+    if (prepare(L, ph, &pv, dtype, H, W, inverse, il_in, il_out, st) == ST_OK) {
+      L.a.in = x;
+      L.a.out = y;
+      L.a.rows = nblk * H;
+      L.a.frames = frames;
+      L.a.frame_h = fh;
+      L.a.frame_w = fw;
+      rc = L.k->fn(L.a);
+      if (rc != ST_ERR_UNSUPPORTED) {
+        int rc2 = finish(L, st);
+        return rc ? rc : rc2;
+      }
+    }
+    L = Launch();
+  }
   rc = prepare(L, ph, &pv, dtype, H, W, inverse, in_mode, out_mode, st);
   if (rc == ST_ERR_UNSUPPORTED) {
     // dense composite of both axes: one fused kernel per shape is always built

@@ -56,7 +56,21 @@ template <typename T, int H, int W, int P, int MODE>
 int make_map(CUtensorMap* map, const void* base, const LaunchArgs& a) {
   using L = TileLayout<T, H, W, P>;
   constexpr int dt = sizeof(T) == 4 ? DT_F32 : DT_F64;
-  if constexpr (MODE == MODE_LINEAR || MODE == MODE_GATHER) {
+  if constexpr (MODE == MODE_LINEAR_IL) {  // (nblk, H, W) as {W, block, row}
+    uint64_t dims[3] = {static_cast<uint64_t>(W), static_cast<uint64_t>(a.rows / H),
+                        static_cast<uint64_t>(H)};
+    uint64_t strides[2] = {static_cast<uint64_t>(H) * W * sizeof(T), static_cast<uint64_t>(W) * sizeof(T)};
+    uint32_t box[3] = {static_cast<uint32_t>(W), static_cast<uint32_t>(P), static_cast<uint32_t>(H)};
+    return encode_tensor_map(map, dt, 3, dims, strides, box, L::BRB, const_cast<void*>(base));
+  } else if constexpr (MODE == MODE_FRAME_IL) {  // {W, block column, frame row, frame}
+    uint64_t dims[4] = {static_cast<uint64_t>(W), static_cast<uint64_t>(a.frame_w / W),
+                        static_cast<uint64_t>(a.frame_h), static_cast<uint64_t>(a.frames)};
+    uint64_t strides[3] = {static_cast<uint64_t>(W) * sizeof(T),
+                           static_cast<uint64_t>(a.frame_w) * sizeof(T),
+                           static_cast<uint64_t>(a.frame_w) * a.frame_h * sizeof(T)};
+    uint32_t box[4] = {static_cast<uint32_t>(W), static_cast<uint32_t>(P), static_cast<uint32_t>(H), 1u};
+    return encode_tensor_map(map, dt, 4, dims, strides, box, L::BRB, const_cast<void*>(base));
+  } else if constexpr (MODE == MODE_LINEAR || MODE == MODE_GATHER) {
     uint64_t dims[2] = {static_cast<uint64_t>(W), static_cast<uint64_t>(a.rows)};
     uint64_t strides[1] = {static_cast<uint64_t>(W) * sizeof(T)};
     uint32_t box[2] = {static_cast<uint32_t>(L::BW),
@@ -81,8 +95,13 @@ int launch_tile(const LaunchArgs& a) {
   using ColOp = AxisOp<T, H, CC>;
   static_assert(S >= 2, "ring needs at least two stages");
 
+  constexpr bool FR = IN_MODE == MODE_FRAME || OUT_MODE == MODE_FRAME ||
+                      IN_MODE == MODE_FRAME_IL || OUT_MODE == MODE_FRAME_IL;
+  if constexpr (is_il_mode<IN_MODE>()) {
+    if ((a.frame_w / W) % P != 0) return ST_ERR_UNSUPPORTED;  // caller falls back to FRAME
+  }
   Geom g{};
-  if (IN_MODE == MODE_FRAME || OUT_MODE == MODE_FRAME) {
+  if (FR) {
     g.tiles_y = (a.frame_h + H - 1) / H;
     g.tiles_x = a.frame_w / W;
     g.nblocks = static_cast<int64_t>(a.frames) * g.tiles_y * g.tiles_x;
@@ -101,7 +120,7 @@ int launch_tile(const LaunchArgs& a) {
 
   // the LINEAR side of a frame launch holds ntiles whole blocks
   LaunchArgs la = a;
-  if (IN_MODE == MODE_FRAME || OUT_MODE == MODE_FRAME) la.rows = g.nblocks * H;
+  if (FR) la.rows = g.nblocks * H;
 
   CUtensorMap in_map, out_map;
   int rc = make_map<T, H, W, P, IN_MODE>(&in_map, a.in, la);

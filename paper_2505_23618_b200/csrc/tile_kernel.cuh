@@ -175,7 +175,23 @@ struct TileLayout {
 // adjacent blocks moves as ONE 4-D box {32 cols, 4 blocks, 32 rows, 1 frame}, so
 // each frame row is a single 512-byte segment; the smem tile is then row-
 // interleaved (tile row = 4 * block row + block) instead of block-major.
-enum Mode : int { MODE_LINEAR = 0, MODE_FRAME = 1, MODE_GATHER = 2, MODE_FRAME4 = 3 };
+//
+// MODE_FRAME_IL / MODE_LINEAR_IL (tile kernel, rows of <= 128 bytes): the same
+// idea for a P-block super-tile -- the frame side is one 4-D box {W, P blocks,
+// H rows, 1}, the block-major side one 3-D box {W, P blocks, H rows} over
+// (nblk, H, W) -- and both sides see the row-interleaved smem tile.
+enum Mode : int {
+  MODE_LINEAR = 0,
+  MODE_FRAME = 1,
+  MODE_GATHER = 2,
+  MODE_FRAME4 = 3,
+  MODE_FRAME_IL = 4,
+  MODE_LINEAR_IL = 5
+};
+template <int MODE>
+__host__ __device__ constexpr bool is_il_mode() {
+  return MODE == MODE_FRAME_IL || MODE == MODE_LINEAR_IL;
+}
 
 struct Geom {
   int64_t ntiles;      // super-tiles
@@ -213,7 +229,7 @@ DA_DEV void gather_io(bool load, void* stage, const CUtensorMap* map, uint64_t* 
 // Blocks of super-tile t that exist (a FRAME super-tile may be cut short).
 template <int P, int MODE>
 DA_DEV int tile_blocks(int64_t t, const Geom& g) {
-  if constexpr (MODE == MODE_LINEAR) {
+  if constexpr (MODE == MODE_LINEAR || is_il_mode<MODE>()) {
     return P;
   } else {
     const int64_t left = g.nblocks - t * P;
@@ -229,6 +245,26 @@ template <typename T, int H, int W, int P, int MODE, int CH = 0>
 DA_DEV void issue_tile_io(bool load, void* stage, const CUtensorMap* map, uint64_t* bar,
                           int64_t t, const Geom& g, int nb) {
   using L = TileLayout<T, H, W, P>;
+  if constexpr (is_il_mode<MODE>()) {
+    static_assert(L::NB == 1, "interleaved tiles need rows of <= 128 bytes");
+    if constexpr (MODE == MODE_LINEAR_IL) {
+      const int b0 = static_cast<int>(t * P);
+      if (load)
+        tma_load_3d(stage, map, bar, 0, b0, 0);
+      else
+        tma_store_3d(map, stage, 0, b0, 0);
+    } else {
+      const int64_t per = static_cast<int64_t>(g.tiles_x) * g.tiles_y, blk = t * P;
+      const int f = static_cast<int>(blk / per);
+      const int rem = static_cast<int>(blk - f * per);
+      const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+      if (load)
+        tma_load_4d(stage, map, bar, 0, tx, ty * H, f);
+      else
+        tma_store_4d(map, stage, 0, tx, ty * H, f);
+    }
+    return;
+  }
 #pragma unroll
   for (int b = 0; b < L::NB; ++b) {
     uint8_t* dst = static_cast<uint8_t*>(stage) + b * L::BOXB;
@@ -342,10 +378,13 @@ DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Co
 
 // Column pass: lane owns a column (PAIR: two adjacent columns read as one
 // 8-byte word, packed as f2 lanes).  Conflict-free under the swizzle.
-template <typename T, int H, int W, int P, int CC, int GSQ, bool PAIR, int GT = 32>
+template <typename T, int H, int W, int P, int CC, int GSQ, bool PAIR, int GT = 32,
+          bool IL = false>
 DA_DEV void col_pass(uint8_t* buf, int lane, const typename AxisOp<T, H, CC>::Coef& cf,
                      const T* dense) {
   using L = TileLayout<T, H, W, P>;
+  // tile row of (block p, block row i): block-major, or row-interleaved (IL)
+  auto row = [](uint32_t p, uint32_t i) { return IL ? i * P + p : p * H + i; };
   constexpr int COLS_PER_IT = PAIR ? 2 * GT : GT;
   static_assert((P * W) % COLS_PER_IT == 0, "column pass must cover whole warps");
 #pragma unroll 1
@@ -357,22 +396,22 @@ DA_DEV void col_pass(uint8_t* buf, int lane, const typename AxisOp<T, H, CC>::Co
       T v[H];
 #pragma unroll
       for (int i = 0; i < H; ++i)
-        v[i] = *reinterpret_cast<const T*>(buf + L::addr(p * H + i, byte));
+        v[i] = *reinterpret_cast<const T*>(buf + L::addr(row(p, i), byte));
       apply_axis<T, H, CC>(v, cf, dense);
       scale_out<T, H, GSQ>(v);
 #pragma unroll
-      for (int i = 0; i < H; ++i) *reinterpret_cast<T*>(buf + L::addr(p * H + i, byte)) = v[i];
+      for (int i = 0; i < H; ++i) *reinterpret_cast<T*>(buf + L::addr(row(p, i), byte)) = v[i];
     } else {
       static_assert(sizeof(T) == 4, "packed columns are fp32 pairs");
       f2 v[H];
 #pragma unroll
       for (int i = 0; i < H; ++i)
-        v[i].v = *reinterpret_cast<const float2*>(buf + L::addr(p * H + i, byte));
+        v[i].v = *reinterpret_cast<const float2*>(buf + L::addr(row(p, i), byte));
       apply_axis<f2, H, CC>(v, cf, dense);
       scale_out<f2, H, GSQ>(v);
 #pragma unroll
       for (int i = 0; i < H; ++i)
-        *reinterpret_cast<float2*>(buf + L::addr(p * H + i, byte)) = v[i].v;
+        *reinterpret_cast<float2*>(buf + L::addr(row(p, i), byte)) = v[i].v;
     }
   }
 }
@@ -446,6 +485,8 @@ __global__ void __launch_bounds__(NG * NW * 32)
 
   constexpr bool GATHER = IN_MODE == MODE_GATHER;
   static_assert(GATHER == (OUT_MODE == MODE_GATHER), "gather mode is in+out");
+  constexpr bool IL = is_il_mode<IN_MODE>();
+  static_assert(IL == is_il_mode<OUT_MODE>(), "interleaved tiles are in+out");
   static_assert(!GATHER || P <= GT, "one thread per gathered block");
   // GATHER: the offsets of the blocks in flight (stage-major) and a register
   // prefetch of the next refill's offsets, one lane per block
@@ -497,11 +538,11 @@ __global__ void __launch_bounds__(NG * NW * 32)
         if constexpr (!ColOp::kIdentity) group_sync<NW>(grp);
       }
       if constexpr (!ColOp::kIdentity)
-        col_pass<T, H, W, P, CC, GSQ, PAIR_COL, GT>(buf, lane, prm.col, dense_col);
+        col_pass<T, H, W, P, CC, GSQ, PAIR_COL, GT, IL>(buf, lane, prm.col, dense_col);
     } else {
       if constexpr (!ColOp::kIdentity) {
-        col_pass<T, H, W, P, CC, RowOp::kIdentity ? GSQ : 1, PAIR_COL, GT>(buf, lane, prm.col,
-                                                                          dense_col);
+        col_pass<T, H, W, P, CC, RowOp::kIdentity ? GSQ : 1, PAIR_COL, GT, IL>(buf, lane, prm.col,
+                                                                              dense_col);
         if constexpr (!RowOp::kIdentity) group_sync<NW>(grp);
       }
       if constexpr (!RowOp::kIdentity)

@@ -483,3 +483,28 @@ def test_dense_tc_frames_4wide(shape):
     assert rel_err(y.cpu().numpy(), want) < F32_TOL
     back = pipeline.inverse_frames(th, tv, y, h, w).cpu().numpy()
     assert rel_err(back.reshape(f, h, w), fr) < F32_TOL
+
+
+def _frame_tiles(fr, ty, tx):
+    f, h, w = fr.shape
+    pad = np.zeros((f, ty * 32, tx * 32))
+    pad[:, :h, :w] = fr
+    return pad.reshape(f, ty, 32, tx, 32).transpose(0, 1, 3, 2, 4).reshape(-1, 32, 32)
+
+
+@pytest.mark.parametrize("shape", [(2, 70, 128), (1, 64, 64), (3, 40, 192), (2, 33, 96)])
+@pytest.mark.parametrize("name", ["sub8_post_dct2_dst7_n32", "band6_pre_dst3_dst7_n32"])
+def test_frames_interleaved_and_fallback(shape, name):
+    """Frame widths holding whole super-tiles take the interleaved one-box path
+    (FRAME_IL / LINEAR_IL); odd block counts per row (96 = 3 blocks) fall back to
+    per-block boxes.  Oracle parity forward, exact round trip back."""
+    adj = matio.load_designed(name)
+    t = pipeline.make_adjusted_transform(adj)
+    f, h, w = shape
+    fr = np.round(np.random.default_rng(w + h).standard_normal(shape) * 40)
+    y = pipeline.forward_frames(t, t, dev(fr))
+    ax = oaxis(adj)
+    want = O.adjusted_2d(ax, ax, _frame_tiles(fr, -(-h // 32), w // 32))
+    assert rel_err(y.cpu().numpy(), want) < F32_TOL
+    back = pipeline.inverse_frames(t, t, y, h, w)
+    assert torch.equal(torch.round(back), dev(fr))

@@ -182,6 +182,9 @@ def instances():
         p, ng, s, pr = tile_config("float", 32, 32, True, cf, rc)
         in_mode, out_mode = (0, 1) if cf else (1, 0)
         out.append(("float", 32, 32, p, rc, cc, cf, in_mode, out_mode, ng, s, pr))
+        # one-box-per-super-tile interleaved variant (frame width a multiple of P blocks)
+        in_mode, out_mode = (5, 4) if cf else (4, 5)
+        out.append(("float", 32, 32, p, rc, cc, cf, in_mode, out_mode, ng, s, pr))
     # mixed-shape gather kernels (config 3): fp32, the four C3 shapes, pre + post
     for h, w in ((16, 16), (16, 32), (32, 16), (32, 32)):
         for rc, cc, cf in two_d_pairs():
