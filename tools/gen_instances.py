@@ -148,6 +148,8 @@ EXPERIMENT = {
                (2, 3, 2, False, False, 0, 4), (2, 2, 3, False, False, 0, 4)],
 }
 EXPERIMENT_OPS = None  # filled below: the band-6 and sub-8 2-D ops
+# interleaved frame kernels (config 5): (P, NG, S); pair flags as the default
+FRAME_IL_EXPERIMENT = [(4, 2, 3), (2, 4, 6), (4, 3, 3), (4, 4, 2), (8, 2, 3)]
 
 
 def instances():
@@ -182,9 +184,11 @@ def instances():
         p, ng, s, pr = tile_config("float", 32, 32, True, cf, rc)
         in_mode, out_mode = (0, 1) if cf else (1, 0)
         out.append(("float", 32, 32, p, rc, cc, cf, in_mode, out_mode, ng, s, pr))
-        # one-box-per-super-tile interleaved variant (frame width a multiple of P blocks)
+        # one-box-per-super-tile interleaved variant (frame width a multiple of P
+        # blocks): 16 KB super-tiles (512-byte frame-row segments), 4 warps x 3
+        # stages -- measured best on B200 (forward at the HBM roofline)
         in_mode, out_mode = (5, 4) if cf else (4, 5)
-        out.append(("float", 32, 32, p, rc, cc, cf, in_mode, out_mode, ng, s, pr))
+        out.append(("float", 32, 32, 4, rc, cc, cf, in_mode, out_mode, 4, 3, pr))
     # mixed-shape gather kernels (config 3): fp32, the four C3 shapes, pre + post
     for h, w in ((16, 16), (16, 32), (32, 16), (32, 32)):
         for rc, cc, cf in two_d_pairs():
@@ -207,6 +211,10 @@ def instances():
             final.append(inst[:11] + (False, False, 0, 0, 2))
             continue
         final.append(inst[:11] + (pr and cc != ID, pc, 0, 0))
+        if (dt, h, w) == ("float", 32, 32) and (im, om) in ((4, 5), (5, 4)):
+            for k, (pp, nng, ss) in enumerate(FRAME_IL_EXPERIMENT, start=1):
+                _, ppc = pair_flags(dt, h, w, pp, rc, cc)
+                final.append((dt, h, w, pp, rc, cc, cf, im, om, nng, ss, pr and cc != ID, ppc, k, 0, 1))
         if (dt, h, w) in EXPERIMENT and im == 0 and om == 0 and rc == cc \
                 and rc in (code(DCT2, SUB, 8), code(SUB, IDCT2, 8), code(GIVENS, DST3, 6),
                            code(IDST3, GIVENS, 6)):
