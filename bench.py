@@ -219,6 +219,7 @@ class Uniform(Workload):
             _lib.check(lib.dctadj_inverse_2d(ref, ref, self.y.data_ptr(), self.xr.data_ptr(), nblk, dtc, st))
 
         self.launches = [("forward_2d", fwd)] + ([("inverse_2d", inv)] if inverse else [])
+        self._lib, self._dtc, self._st, self._ref = lib, dtc, st, ref
         # e2e: the same step through the host-buffer entries (pinned arrays)
         self.xh = self.x.cpu().pin_memory().numpy()
         self.yh = torch.empty(tuple(self.x.shape), dtype=self.x.dtype).pin_memory().numpy()
@@ -235,6 +236,25 @@ class Uniform(Workload):
         self.extra = {"blocks_per_gpu": nblk, "block": f"{n}x{n}",
                       "l2": f"inputs {nb / 1e6:.0f} MB per GPU "
                             + ("> 126 MB L2; no flush" if nb > 126e6 else "< 126 MB L2: L2-resident")}
+
+    def rotating(self, min_bytes: float = 1.0e9):
+        """L2-resident configs (C1): step functions over R distinct input/output
+        buffer pairs, R chosen so one cycle moves >= min_bytes (8x the 126 MB L2);
+        the survey asks for this number beside the resident one."""
+        import torch
+        from paper_2505_23618_b200 import _lib
+        nb = self.x.numel() * self.x.element_size()
+        r = max(2, int(np.ceil(min_bytes / (2 * nb))))
+        xs = [self.x.clone() for _ in range(r)]
+        ys = [torch.empty_like(self.x) for _ in range(r)]
+        lib, dtc, st, ref, nblk = self._lib, self._dtc, self._st, self._ref, self.nblk
+
+        def step(i):
+            _lib.check(lib.dctadj_forward_2d(ref, ref, xs[i].data_ptr(), ys[i].data_ptr(), nblk, dtc, st))
+            if self.inverse:
+                _lib.check(lib.dctadj_inverse_2d(ref, ref, ys[i].data_ptr(), xs[i].data_ptr(), nblk,
+                                                 dtc, st))
+        return r, step
 
     def gate(self):
         import torch
@@ -535,6 +555,37 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         per_launch_ms.append(a.elapsed_time(b) / reps)
 
+    # dispersion: per-step CUDA events over up to 50 further steps (median, IQR)
+    nsamp = min(args.steps, 50)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(nsamp + 1)]
+    ev[0].record(stream)
+    for i in range(nsamp):
+        for _, fn in w.launches:
+            fn()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    step_ms = np.array([ev[i].elapsed_time(ev[i + 1]) for i in range(nsamp)])
+    q1, med, q3 = np.percentile(step_ms, [25, 50, 75])
+    dispersion = {"median_ms_per_step": float(med), "iqr_ms": float(q3 - q1), "samples": nsamp,
+                  "note": "per-step events (separate pass after the timed region)"}
+
+    rot = None
+    if isinstance(w, Uniform) and w.bytes_first_launch < 126e6:
+        nbuf, step = w.rotating()
+        for i in range(nbuf):
+            step(i)
+        torch.cuda.synchronize()
+        nrot = max(args.steps, 2 * nbuf)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(nrot):
+            step(i % nbuf)
+        b.record(stream)
+        torch.cuda.synchronize()
+        rms = a.elapsed_time(b) / nrot
+        rot = {"value": w.coef_per_step / (rms / 1e3), "ms_per_step": rms, "buffers": nbuf,
+               "note": "inputs rotate over buffers totalling > 8x L2 (not L2-resident)"}
+
     e2e_s = None
     if w.e2e is not None:
         w.e2e()  # warm
@@ -566,6 +617,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     config = {"workload": w.workload, "parallelism": f"block-range shards x{world}",
               "oracle_gate_rel_err": err}
     config.update(w.extra)
+    if rot is not None:
+        config["l2_rotating_buffers"] = rot
     if approx is not None:
         config["approx_error_vs_exact_dst7_all_tiles"] = approx[0] / approx[1]
         config["approx_error_vs_exact_dst7_unpadded_tile_rows"] = approx[2] / approx[3]
@@ -588,6 +641,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 if e2e_s else None),
         "gpu_launches": args.steps * (w.kernels_per_step or nl),
         "clocks": clk.summary(),
+        "dispersion": dispersion,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_throughput(args.config, seconds=args.cpu_seconds)
