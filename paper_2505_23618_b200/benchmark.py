@@ -13,6 +13,8 @@ the reference's 1-D batches the 2-D block transforms are measured too.
 """
 from __future__ import annotations
 
+import contextlib
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -62,6 +64,21 @@ def _dense_transform(h: np.ndarray):
     return pipeline.make_adjusted_transform(rec)
 
 
+@contextlib.contextmanager
+def dense_on_cuda_cores():
+    """Route dense 2-D transforms to the CUDA-core FMA kernel (DCTADJ_DENSE_TC=0,
+    read by the library per call) -- the reference's full-matrix product."""
+    old = os.environ.get("DCTADJ_DENSE_TC")
+    os.environ["DCTADJ_DENSE_TC"] = "0"
+    try:
+        yield
+    finally:
+        if old is None:
+            del os.environ["DCTADJ_DENSE_TC"]
+        else:
+            os.environ["DCTADJ_DENSE_TC"] = old
+
+
 def _measure(fn, samples: int, warmup: int):
     import torch
     for _ in range(warmup):
@@ -70,6 +87,9 @@ def _measure(fn, samples: int, warmup: int):
     times = np.empty(samples)
     for i in range(samples):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # keep the device busy (~1 ms) while the host enqueues the call, so the
+        # events bracket the kernels rather than the Python / ctypes overhead
+        torch.cuda._sleep(2_000_000)
         e0.record()
         fn()
         e1.record()
@@ -117,9 +137,16 @@ def run_benchmark(pipelines=DEFAULT_PIPELINES, sizes=(32, 64), samples: int = 31
                 dinv = lambda: pipeline.inverse_adjusted_2d(td, td, x)   # noqa: E731
             dense_med = {}
             for direction, fn in (("forward", dfwd), ("inverse", dinv)):
-                med, disp = _stats(_measure(fn, samples, warmup), coeffs)
+                # the paper's full-matrix baseline: the FMA matrix product (CUDA cores)
+                with dense_on_cuda_cores():
+                    med, disp = _stats(_measure(fn, samples, warmup), coeffs)
                 dense_med[direction] = med
                 reports.append(BenchReport("dense", size, direction, med, 1.0, samples, disp, layout))
+                if layout == "2d" and size == 32 and dtype == "float32":
+                    # the same product on the tensor cores (3xTF32 tcgen05, dense_tc.cuh)
+                    med, disp = _stats(_measure(fn, samples, warmup), coeffs)
+                    reports.append(BenchReport("dense_tc", size, direction, med,
+                                               med / dense_med[direction], samples, disp, layout))
             for name in pipelines:
                 if name == "multiple":
                     continue
@@ -147,13 +174,14 @@ def run_benchmark(pipelines=DEFAULT_PIPELINES, sizes=(32, 64), samples: int = 31
                     reports.append(BenchReport(name, size, direction, med,
                                                med / dense_med[direction], samples, disp, layout))
         if "multiple" in pipelines:
-            reports.append(_bench_multiple(adj["subblock8"], x2, samples, warmup, tol))
+            reports.extend(_bench_multiple(adj["subblock8"], x2, samples, warmup, tol))
     return reports
 
 
 def _bench_multiple(sub_adj, blocks, samples, warmup, tol) -> BenchReport:
     """Shared five-output encoder evaluation vs five independent dense
     separable 2-D transforms (reference benchmark.py:206-238)."""
+    import torch
     ctx = pipeline.EncoderContext(horizontal=sub_adj, vertical=sub_adj)
     shared = pipeline.simultaneous_encoder_eval(blocks[:8], ctx)
     naive = pipeline.naive_encoder_eval(blocks[:8], ctx)
@@ -163,11 +191,19 @@ def _bench_multiple(sub_adj, blocks, samples, warmup, tol) -> BenchReport:
             raise AssertionError("shared encoder path failed its oracle check")
     coeffs = 5 * blocks.numel()
     t_s = _measure(lambda: pipeline.simultaneous_encoder_eval(blocks, ctx), samples, warmup)
-    t_n = _measure(lambda: pipeline.naive_encoder_eval(blocks, ctx), samples, warmup)
+    with dense_on_cuda_cores():
+        t_n = _measure(lambda: pipeline.naive_encoder_eval(blocks, ctx), samples, warmup)
     med_s, disp = _stats(t_s, coeffs)
     med_n, _ = _stats(t_n, coeffs)
-    return BenchReport("multiple", sub_adj.pattern.size, "forward", med_s, med_s / med_n,
-                       samples, disp, "2d")
+    out = [BenchReport("multiple", sub_adj.pattern.size, "forward", med_s, med_s / med_n,
+                       samples, disp, "2d")]
+    if sub_adj.pattern.size == 32 and blocks.dtype == torch.float32:
+        # the naive side's five dense transforms on the tensor cores instead
+        med_t, _ = _stats(_measure(lambda: pipeline.naive_encoder_eval(blocks, ctx), samples,
+                                   warmup), coeffs)
+        out.append(BenchReport("multiple_vs_tc", sub_adj.pattern.size, "forward", med_s,
+                               med_s / med_t, samples, disp, "2d"))
+    return out
 
 
 def report_table(reports: list[BenchReport], layout: str | None = None) -> str:

@@ -461,13 +461,11 @@ static int primitive(int stage, const void* x, void* y, int64_t nvec, int n, int
 }
 
 // ------------------------------------------------------------- dense on tensor cores
-// DCTADJ_DENSE_TC=0 keeps the dense comparison path on the CUDA-core kernel
+// DCTADJ_DENSE_TC=0 keeps the dense comparison path on the CUDA-core kernel (read
+// per call: the Table-1 harness times both; getenv is a few ns beside a launch)
 static bool dense_tc_enabled() {
-  static bool v = [] {
-    const char* s = std::getenv("DCTADJ_DENSE_TC");
-    return !(s && s[0] == '0');
-  }();
-  return v;
+  const char* s = std::getenv("DCTADJ_DENSE_TC");
+  return !(s && s[0] == '0');
 }
 
 // one zeroed [next, done] counter pair per (device, stream): launches on one stream
