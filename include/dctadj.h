@@ -128,6 +128,21 @@ int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void
                           void* frames, int32_t nframes, int32_t height, int32_t width,
                           int32_t dtype, void* stream);
 
+/* Config 5's comparison step in one call: the adjusted forward (h, v) AND the
+ * exact forward (eh, ev; typically dense DST-7) of the same frames, plus the
+ * per-frame approximation error err[f*4 + {0,1,2,3}] = {sum (Ya - Ye)^2,
+ * sum Ye^2} over all tiles and over tile rows entirely inside `height` (err may
+ * be NULL; it is zeroed first).  fp32 32x32 with a sub-block-8 post or band-6
+ * (Givens) pre adjustment on both axes, dense exact axes and width a multiple of
+ * 128 runs as ONE tensor-core kernel that reads the frames once
+ * (csrc/dense_tc.cuh, FUSED); anything else runs the two frame transforms and a
+ * reduction.  Replaces the reference's two transform calls plus its error sum
+ * (reference pipeline.py:176-199). */
+int dctadj_forward_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dctadj_axis* eh,
+                                const dctadj_axis* ev, const void* frames, void* coefs,
+                                void* exact, double* err, int32_t nframes, int32_t height,
+                                int32_t width, int32_t dtype, void* stream);
+
 /* ---- simultaneous encoder evaluation (reference pipeline.py:256-293, paper
  * Table 1 "Multiple"): for each (H, W) block, one read, one shared 2-D DCT-2 and
  * five coefficient planes, planes[k] (device, each (nblk, H, W)):

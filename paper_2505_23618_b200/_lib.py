@@ -71,6 +71,7 @@ SIGNATURES = {
     "dctadj_inverse_2d_host": [_AP, _AP, _P, _P, _I64, _I32, _I32],
     "dctadj_forward_frames": [_AP, _AP, _P, _P, _I32, _I32, _I32, _I32, _P],
     "dctadj_inverse_frames": [_AP, _AP, _P, _P, _I32, _I32, _I32, _I32, _P],
+    "dctadj_forward_frames_exact": [_AP, _AP, _AP, _AP, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P],
     "dctadj_copy_tiles": [_P, _P, _I64, _I32, _I32, _I32, _P],
     "dctadj_encoder_eval": [_AP, _AP, _P, ctypes.POINTER(_P), _I64, _I32, _P],
     "dctadj_mixed_create": [_P, _P, _P, _I64, _P, _I32, _I64, ctypes.POINTER(_P)],

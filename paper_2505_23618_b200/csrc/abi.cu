@@ -489,8 +489,18 @@ static int stream_sched_counter(cudaStream_t st, unsigned long long** out) {
   return ST_OK;
 }
 
-template <int IN_MODE, int OUT_MODE>
-static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, int tiles_x) {
+// fused config-5 launch: the adjusted transform's output, packed coefficients
+// (already in fp32) and the per-frame error accumulator
+struct FusedArgs {
+  void* adj_out;
+  const void* row_coef;
+  const void* col_coef;
+  double* err;
+};
+
+template <int IN_MODE, int OUT_MODE, int FRC = 0, int FCC = 0>
+static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, int tiles_x,
+                           const FusedArgs* fz = nullptr) {
   constexpr int S = 8;  // ring of 8 x 16 KB + 4 group tiles x 16 KB: 208 KB, one CTA/SM
   Geom g{};
   g.nblocks = nblocks;
@@ -515,8 +525,20 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   int rc = map_for(&in_map, a.in, IN_MODE);
   if (!rc) rc = map_for(&out_map, a.out, OUT_MODE);
   if (rc) return rc;
+  CUtensorMap adj_map = in_map;  // unused unless fused
+  KParams<float, 32, 32, FRC, FCC> kp;
+  std::memset(&kp, 0, sizeof(kp));
   DenseTcParams prm{static_cast<const float*>(a.dense_row), static_cast<const float*>(a.dense_col),
-                    nullptr, nullptr};
+                    nullptr, nullptr, nullptr, a.frame_h};
+  if constexpr (FRC != 0) {
+    if (!fz) return fail(ST_ERR_VALUE, "fused launch without its arguments");
+    if ((rc = make_map<float, 32, 32, 4, MODE_LINEAR_IL>(&adj_map, fz->adj_out, la))) return rc;
+    using RowOp = AxisOp<float, 32, FRC>;
+    using ColOp = AxisOp<float, 32, FCC>;
+    if (RowOp::NCOEF > 0) std::memcpy(kp.row.c, fz->row_coef, sizeof(float) * RowOp::NCOEF);
+    if (ColOp::NCOEF > 0) std::memcpy(kp.col.c, fz->col_coef, sizeof(float) * ColOp::NCOEF);
+    prm.err = fz->err;
+  }
   int rc_s = stream_sched_counter(a.stream, &prm.sched);
   if (rc_s) return rc_s;
   // diagnostics: DCTADJ_TC_TRACE=<file> dumps CTA 0's per-tile event clocks
@@ -527,25 +549,26 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
     DA_CUDA(cudaMalloc(&prm.trace, trace_bytes));
     DA_CUDA(cudaMemsetAsync(prm.trace, 0, trace_bytes, a.stream));
   }
-  auto kern = dense_tc_kernel<S, IN_MODE, OUT_MODE>;
-  const size_t smem =
-      1024 + S * 16384 + kDenseTcGroups * 16384 + 16384 + (2 * S + 4 * kDenseTcGroups) * 8 +
-      (S + 1) * 8 + 16;
+  constexpr int NG = kDenseTcGroups;
+  constexpr int NTHR = (4 * NG + 3) * 32;
+  auto kern = dense_tc_kernel<S, IN_MODE, OUT_MODE, FRC, FCC, NG>;
+  const size_t smem = 1024 + S * 16384 + NG * 16384 + 16384 + (2 * S + 4 * NG) * 8 + (S + 1) * 8 +
+                      NG * 16 * 8 + 16;
   static int bps = 0;
   if (!bps) {
     DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared));
-    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kDenseTcThreads, smem));
+    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NTHR, smem));
     if (bps < 1) return fail(ST_ERR_CUDA, "dense tensor-core kernel does not fit an SM");
-    bps = std::min(bps, 512 / (128 * kDenseTcGroups));  // TMEM columns per SM
+    bps = 1;  // the kernel allocates all 512 TMEM columns
     if (trace_on())
       std::fprintf(stderr, "[dctadj] dense_tc: %zu B smem, %d CTAs/SM\n", smem, bps);
   }
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * bps;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(g.ntiles, cap)));
-  cfg.blockDim = dim3(kDenseTcThreads);
+  cfg.blockDim = dim3(NTHR);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = a.stream;
   cudaLaunchAttribute attr[1];
@@ -553,7 +576,7 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm));
+  DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm, adj_map, kp));
   if (trace_file) {
     std::vector<unsigned long long> h(kTcTraceTiles * kTcTraceEv + 2 * kTcTraceCtas);
     DA_CUDA(cudaMemcpyAsync(h.data(), prm.trace, trace_bytes, cudaMemcpyDeviceToHost, a.stream));
@@ -762,6 +785,130 @@ static int run_frames(const dctadj_axis* h, const dctadj_axis* v, const void* in
   const int64_t nblk = static_cast<int64_t>(nframes) * ((height + v->n - 1) / v->n) * (width / h->n);
   return run_2d(h, v, in, out, nblk, dtype, inverse, inverse ? MODE_LINEAR : MODE_FRAME,
                 inverse ? MODE_FRAME : MODE_LINEAR, nframes, height, width, st);
+}
+
+// ------------------------------------------------------------- frames: adjusted + exact
+// Per-frame approximation error of adjusted vs exact coefficient blocks (the
+// unfused path).  One warp walks a contiguous run of blocks; lane sums are
+// flushed (warp-reduced, fp64 atomics) when the frame changes.
+template <typename T>
+__global__ void frame_err_kernel(const T* __restrict__ ya, const T* __restrict__ ye, double* err,
+                                 int64_t nblk, int64_t per_frame, int tiles_x, int full_tile_rows,
+                                 int64_t blocks_per_warp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t b0 = warp * blocks_per_warp;
+  const int64_t b1 = b0 + blocks_per_warp < nblk ? b0 + blocks_per_warp : nblk;
+  double acc[4] = {0, 0, 0, 0};
+  int cur = -1;
+  auto flush = [&]() {
+    for (int i = 0; i < 4; ++i) {
+      double a = acc[i];
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0 && cur >= 0) atomicAdd(err + 4 * cur + i, a);
+      acc[i] = 0;
+    }
+  };
+  for (int64_t blk = b0; blk < b1; ++blk) {
+    const int f = static_cast<int>(blk / per_frame);
+    const int ty = static_cast<int>((blk - f * per_frame) / tiles_x);
+    if (f != cur) {
+      flush();
+      cur = f;
+    }
+    double d2 = 0, e2 = 0;
+    for (int i = lane; i < 1024; i += 32) {
+      const double e = static_cast<double>(ye[blk * 1024 + i]);
+      const double d = static_cast<double>(ya[blk * 1024 + i]) - e;
+      d2 += d * d;
+      e2 += e * e;
+    }
+    acc[0] += d2;
+    acc[1] += e2;
+    if (ty < full_tile_rows) {
+      acc[2] += d2;
+      acc[3] += e2;
+    }
+  }
+  flush();
+}
+
+static int run_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dctadj_axis* eh,
+                            const dctadj_axis* ev, const void* frames, void* coefs, void* exact,
+                            double* err, int32_t nframes, int32_t height, int32_t width,
+                            int32_t dtype, cudaStream_t st) {
+  if (!h || !v || !eh || !ev) return fail(ST_ERR_VALUE, "axis descriptor is NULL");
+  if (eh->n != h->n || ev->n != v->n)
+    return fail(ST_ERR_SHAPE, "exact transforms (%d x %d) do not match the adjusted ones (%d x %d)",
+                ev->n, eh->n, v->n, h->n);
+  if (nframes < 0 || height < 0 || width < 0)
+    return fail(ST_ERR_SHAPE, "negative frame geometry %d x %d x %d", nframes, height, width);
+  if (err && nframes > 0) DA_CUDA(cudaMemsetAsync(err, 0, sizeof(double) * 4 * nframes, st));
+  if (nframes == 0 || height == 0 || width == 0) return ST_OK;
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if ((rc = validate_axis(h)) || (rc = validate_axis(v)) || (rc = validate_axis(eh)) ||
+      (rc = validate_axis(ev)))
+    return rc;
+  if (width % h->n != 0)
+    return fail(ST_ERR_SHAPE, "frame width %d is not a multiple of the block width %d", width,
+                h->n);
+  const int ty = (height + v->n - 1) / v->n, tx = width / h->n;
+  const int64_t nblk = static_cast<int64_t>(nframes) * ty * tx;
+  if (!frames || !coefs || !exact) return fail(ST_ERR_VALUE, "NULL data pointer");
+
+  // fused: one read of the frames feeds both transforms and the error sums
+  // (dense_tc.cuh, FUSED).  Without err the two separate launches are faster
+  // (each sits at the HBM roofline; the fused kernel is issue-bound).
+  AxisPlan ph, pv, peh, pev;
+  if (err && dtype == DT_F32 && h->n == 32 && v->n == 32 && tx % 4 == 0 && dense_tc_enabled() &&
+      !plan_axis(h, false, false, &ph) && !plan_axis(v, false, false, &pv) &&
+      !plan_axis(eh, false, true, &peh) && !plan_axis(ev, false, true, &pev) &&
+      peh.code == op_code(ST_DENSE) && pev.code == op_code(ST_DENSE) && ph.code == pv.code) {
+    constexpr int kSub8 = op_code(ST_DCT2, ST_SUB, 8), kGiv6 = op_code(ST_GIVENS, ST_DST3, 6);
+    if (ph.code == kSub8 || ph.code == kGiv6) {
+      Launch L;
+      if ((rc = upload_dense(peh, dtype, st, &L.dense_row)) ||
+          (rc = upload_dense(pev, dtype, st, &L.dense_col)))
+        return rc;
+      std::vector<unsigned char> rcf = to_dtype(ph.coef, DT_F32), ccf = to_dtype(pv.coef, DT_F32);
+      LaunchArgs a;
+      a.in = frames;
+      a.out = exact;
+      a.frames = nframes;
+      a.frame_h = height;
+      a.frame_w = width;
+      a.dense_row = L.dense_row;
+      a.dense_col = L.dense_col;
+      a.stream = st;
+      FusedArgs fz{coefs, rcf.data(), ccf.data(), err};
+      rc = ph.code == kSub8
+               ? launch_dense_tc<MODE_FRAME4, MODE_LINEAR, kSub8, kSub8>(a, nblk, ty, tx, &fz)
+               : launch_dense_tc<MODE_FRAME4, MODE_LINEAR, kGiv6, kGiv6>(a, nblk, ty, tx, &fz);
+      if (trace_on()) std::fprintf(stderr, "[dctadj] frames_exact: fused (rc %d)\n", rc);
+      return rc;
+    }
+  }
+  // unfused: two frame launches + the error reduction
+  if ((rc = run_frames(h, v, frames, coefs, nframes, height, width, dtype, false, st))) return rc;
+  if ((rc = run_frames(eh, ev, frames, exact, nframes, height, width, dtype, false, st))) return rc;
+  if (err) {
+    if (h->n != 32 || v->n != 32) return ST_OK;  // error sums are defined on 32x32 tiles
+    const int64_t per_warp = 64, warps = (nblk + per_warp - 1) / per_warp;
+    const int grid = static_cast<int>((warps * 32 + 255) / 256);
+    const int full = height / 32;
+    if (dtype == DT_F32)
+      frame_err_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(coefs),
+                                                     static_cast<const float*>(exact), err, nblk,
+                                                     static_cast<int64_t>(ty) * tx, tx, full, per_warp);
+    else
+      frame_err_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(coefs),
+                                                      static_cast<const double*>(exact), err, nblk,
+                                                      static_cast<int64_t>(ty) * tx, tx, full, per_warp);
+    DA_CUDA(cudaGetLastError());
+  }
+  if (trace_on()) std::fprintf(stderr, "[dctadj] frames_exact: unfused\n");
+  return ST_OK;
 }
 
 // ------------------------------------------------------------- encoder evaluation
@@ -1107,6 +1254,13 @@ int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void
                           void* frames, int32_t nframes, int32_t height, int32_t width,
                           int32_t dtype, void* stream) {
   return run_frames(h, v, coefs, frames, nframes, height, width, dtype, true, S(stream));
+}
+int dctadj_forward_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dctadj_axis* eh,
+                                const dctadj_axis* ev, const void* frames, void* coefs,
+                                void* exact, double* err, int32_t nframes, int32_t height,
+                                int32_t width, int32_t dtype, void* stream) {
+  return run_frames_exact(h, v, eh, ev, frames, coefs, exact, err, nframes, height, width, dtype,
+                          S(stream));
 }
 
 int dctadj_copy_tiles(const void* x, void* y, int64_t nblk, int32_t h, int32_t w, int32_t dtype,

@@ -106,6 +106,8 @@ struct DenseTcParams {
   const float* dv;  // device 32x32: column-pass matrix
   unsigned long long* trace;  // diagnostics (DCTADJ_TC_TRACE): CTA 0 event clocks, or null
   unsigned long long* sched;  // [next, done]: dynamic tile counter, zero between launches
+  double* err;     // fused: per frame [sum d^2 all, sum e^2 all, sum d^2 full rows, sum e^2 full]
+  int32_t frame_h; // fused: frame height (tile rows below it are zero-padded)
 };
 constexpr int kTcTraceTiles = 128, kTcTraceEv = 8, kTcTraceCtas = 1024;
 DA_DEV unsigned long long globaltimer() {
@@ -199,12 +201,27 @@ DA_DEV uint32_t tc_row(uint32_t b, uint32_t r) {
 // d2_done per group; a group's threads meet at a named barrier before its
 // elected thread arrives or issues the TMA store of Y (staged in the group's
 // 16 KB smem tile, which also carries the per-warp W transposes).
-template <int S, int IN_MODE, int OUT_MODE>
-__global__ void __launch_bounds__(kDenseTcThreads, 1)
+//
+// FUSED (FRC != 0; config 5): the same launch also runs the ADJUSTED transform
+// (row op FRC, column op FCC, the tile kernel's register butterflies, scalar
+// lanes, 128 threads per group) in place on the loaded frame super-tile while
+// the MMAs are in flight, stores it through adj_map (block-major, interleaved
+// tile), and accumulates the per-frame approximation error of adjusted vs exact
+// coefficients -- one HBM read of the frames for both transforms.
+template <int S, int IN_MODE, int OUT_MODE, int FRC = 0, int FCC = 0, int NGRP = kDenseTcGroups>
+__global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
     dense_tc_kernel(const __grid_constant__ CUtensorMap in_map,
                     const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
-                    const __grid_constant__ DenseTcParams prm) {
-  constexpr int NGRP = kDenseTcGroups;
+                    const __grid_constant__ DenseTcParams prm,
+                    const __grid_constant__ CUtensorMap adj_map,
+                    const __grid_constant__ KParams<float, 32, 32, FRC, FCC> kp) {
+  constexpr int NTHR = (4 * NGRP + 3) * 32;
+  constexpr bool FUSED = FRC != 0;
+  static_assert(!FUSED || (IN_MODE == MODE_FRAME4 && OUT_MODE == MODE_LINEAR),
+                "the fused adjusted + exact path reads frames as one-box super-tiles");
+  using RowOp = AxisOp<float, 32, FRC>;
+  using ColOp = AxisOp<float, 32, FCC>;
+  static_assert(!FUSED || (!RowOp::kDense && !ColOp::kDense), "fused ops are the fast paths");
   static_assert(NGRP * 128 <= 512, "TMEM columns");
   using L = TileLayout<float, 32, 32, 4>;  // 128 rows x 128 B, SW128
   static_assert(L::TILEB == 16384 && L::STAGEB == 16384, "4 blocks of 32x32 fp32");
@@ -225,11 +242,12 @@ __global__ void __launch_bounds__(kDenseTcThreads, 1)
   uint64_t* d2_done = a2_ready + NGRP;
   int64_t* tile_id = reinterpret_cast<int64_t*>(d2_done + NGRP);  // per ring stage; -1 = end
   volatile int64_t* total_k = tile_id + S;  // tiles this CTA got (-1 until known)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_id + S + 1);
+  double* red = reinterpret_cast<double*>(tile_id + S + 1);  // NGRP x 4 warps x 4 (fused)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red + NGRP * 16);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // constant B operands: Dv, Dh split into tf32 hi / lo, K-major SW128 (32 rows)
-  for (int e = tid; e < 1024; e += kDenseTcThreads) {
+  for (int e = tid; e < 1024; e += NTHR) {
     const int r = e >> 5, c = e & 31;
     const float h = prm.dh[e], v = prm.dv[e];
     const uint32_t hh = tc::tf32_hi(h), vh = tc::tf32_hi(v);
@@ -253,10 +271,9 @@ __global__ void __launch_bounds__(kDenseTcThreads, 1)
     fence_mbar_init();
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(128 * NGRP)
-                 : "memory");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");  // all of TMEM (one CTA per SM; NGRP x 128 columns used)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   fence_proxy_async_smem();
@@ -336,6 +353,28 @@ __global__ void __launch_bounds__(kDenseTcThreads, 1)
     uint8_t* gt = gtile + g * 16384;
     const uint32_t ta = tmem + 128 * g + lane_addr;  // this lane's A / D1 / D2 columns
     auto group_bar = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); };
+    // fused: per-thread error sums of the current frame, flushed (group-reduced,
+    // one fp64 atomic per value) when the frame changes and at the end
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int acc_f = -1;
+    auto flush = [&]() {
+      if (acc_f >= 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double a = acc[i];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          if (lane == 0) red[(g * 4 + b) * 4 + i] = a;
+        }
+        group_bar();
+        if (b == 0 && lane < 4)
+          atomicAdd(prm.err + 4 * acc_f + lane, red[(g * 4 + 0) * 4 + lane] + red[(g * 4 + 1) * 4 + lane] +
+                                                    red[(g * 4 + 2) * 4 + lane] + red[(g * 4 + 3) * 4 + lane]);
+        group_bar();
+      }
+      acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+    };
+    int prev_s = -1;  // fused: ring stage still held by the previous tile
     const bool tr = prm.trace && blockIdx.x == 0 && leader;
     auto ev = [&](int64_t k, int e) {
       if (tr && k < kTcTraceTiles) prm.trace[k * kTcTraceEv + e] = clock64();
@@ -343,12 +382,21 @@ __global__ void __launch_bounds__(kDenseTcThreads, 1)
     for (int64_t k = g;; k += NGRP) {
       const int s = static_cast<int>(k % S);
       const uint32_t gp = static_cast<uint32_t>((k / NGRP) & 1);  // this group's use parity
-      const uint8_t* x = stages + s * 16384;
+      uint8_t* x = stages + s * 16384;
       uint32_t v[32];
       // pass-1 A: column j = lane of block b, A[(b,j)][i] = X_b[i][j]
       ev(k, 0);
       mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
       const int64_t t = tile_id[s];
+      if constexpr (FUSED) {
+        // the previous tile's stage carried its adjusted output: free it once both
+        // of that tile's stores have read shared memory
+        if (leader && prev_s >= 0) {
+          bulk_wait_read<0>();
+          mbar_arrive(&empty[prev_s]);
+        }
+        prev_s = s;
+      }
       if (t < 0) break;
       ev(k, 1);
 #pragma unroll
@@ -360,9 +408,17 @@ __global__ void __launch_bounds__(kDenseTcThreads, 1)
       tc::fence_before();
       group_bar();
       if (leader) {
-        mbar_arrive(&empty[s]);
+        if constexpr (!FUSED) mbar_arrive(&empty[s]);  // fused: the stage is still needed
         mbar_arrive(&a1_ready[g]);
       }
+      // fused: the adjusted transform in place on the interleaved tile, its row
+      // pass overlapping MMA pass 1 and its column pass overlapping pass 2 (all 4
+      // warps, scalar lanes: a thread owns one row, then one column)
+      constexpr int GSQ = RowOp::kGainSq * ColOp::kGainSq;
+      const int gl = static_cast<int>(b) * 32 + lane;
+      if constexpr (FUSED)
+        row_pass<float, 32, 32, 4, FRC, ColOp::kIdentity ? GSQ : 1, false, 128>(x, gl, kp.row,
+                                                                               nullptr);
       ev(k, 2);
       // W_b = Dv X_b: lane j holds column j; transpose through this warp's 4 KB
       mbar_wait(&d1_done[g], gp);
@@ -385,12 +441,49 @@ __global__ void __launch_bounds__(kDenseTcThreads, 1)
       tc::fence_before();
       group_bar();
       if (leader) mbar_arrive(&a2_ready[g]);
+      if constexpr (FUSED) {  // (the barrier above also closed the row pass)
+        col_pass<float, 32, 32, 4, FCC, GSQ, false, 128, true>(x, gl, kp.col, nullptr);
+        fence_proxy_async_smem();
+        group_bar();
+        if (leader) {
+          tma_store_3d(&adj_map, x, 0, static_cast<int>(4 * t), 0);
+          bulk_commit();
+        }
+      }
       ev(k, 4);
       // Y_b rows from TMEM into the group tile, TMA store
       mbar_wait(&d2_done[g], gp);
       tc::fence_after();
       ev(k, 5);
       tc::ld32(ta + 96, v);
+      if constexpr (FUSED) {
+        // approximation error of this row: adjusted (stage) vs exact (TMEM)
+        float d2 = 0.f, e2 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 a = *reinterpret_cast<const float4*>(x + tc::sw(lane * 4 + b, q * 4));
+          const float ya[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float ye = __uint_as_float(v[4 * q + u]), d = ya[u] - ye;
+            d2 = fmaf(d, d, d2);
+            e2 = fmaf(ye, ye, e2);
+          }
+        }
+        const int64_t per = static_cast<int64_t>(geom.tiles_x) * geom.tiles_y, blk = 4 * t;
+        const int f = static_cast<int>(blk / per);
+        const int ty = static_cast<int>((blk - f * per) / geom.tiles_x);
+        if (f != acc_f) {
+          flush();
+          acc_f = f;
+        }
+        acc[0] += d2;
+        acc[1] += e2;
+        if ((ty + 1) * 32 <= prm.frame_h) {
+          acc[2] += d2;
+          acc[3] += e2;
+        }
+      }
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         *reinterpret_cast<uint4*>(gt + tc::sw(tc_row<OUT_MODE>(b, lane), q * 4)) =
@@ -404,6 +497,7 @@ __global__ void __launch_bounds__(kDenseTcThreads, 1)
       }
       ev(k, 6);
     }
+    if constexpr (FUSED) flush();
     if (leader) bulk_wait_all();
   }
   tc::fence_before();
@@ -419,9 +513,7 @@ __global__ void __launch_bounds__(kDenseTcThreads, 1)
     }
   }
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(128 * NGRP)
-                 : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 }  // namespace dctadj

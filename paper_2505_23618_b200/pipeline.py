@@ -284,6 +284,34 @@ def forward_frames(th: AdjustedTransform, tv: AdjustedTransform, frames):
     return _device.from_device(y, as_np)
 
 
+def forward_frames_exact(th: AdjustedTransform, tv: AdjustedTransform, eh: AdjustedTransform,
+                         ev: AdjustedTransform, frames, with_error: bool = True):
+    """Config 5's comparison step: adjusted (th, tv) and exact (eh, ev) forward
+    transforms of the same frames plus the per-frame approximation error.
+
+    Returns (y_adj, y_exact, err) with err of shape (F, 4): sum (Ya - Ye)^2 and
+    sum Ye^2 over all tiles, then over the tile rows entirely inside the frame.
+    fp32 32x32 sub8-post / band6-pre with dense exact axes runs as one tensor-
+    core kernel reading the frames once (C-ABI dctadj_forward_frames_exact);
+    with_error=False skips the sums (err is None) and runs the two transforms as
+    separate launches, which is faster when the error is not wanted."""
+    import torch
+    t, as_np = _device.to_device(frames)
+    if t.dim() != 3:
+        raise ShapeError(f"expected (F, height, width) frames, got ndim={t.dim()}")
+    f, hh, ww = t.shape
+    nblk = frame_block_count(f, hh, ww, tv.size, th.size)
+    y = _device.empty_like(t, (nblk, tv.size, th.size))
+    ye = _device.empty_like(t, (nblk, tv.size, th.size))
+    err = torch.empty((f, 4), dtype=torch.float64, device=t.device) if with_error else None
+    axes = [a.axis() for a in (th, tv, eh, ev)]
+    _lib.call("dctadj_forward_frames_exact", *[ctypes.byref(a) for a, _k in axes], t.data_ptr(),
+              y.data_ptr(), ye.data_ptr(), err.data_ptr() if with_error else None, f, hh, ww,
+              _device.dtype_code(t), _device.stream_handle())
+    return (_device.from_device(y, as_np), _device.from_device(ye, as_np),
+            _device.from_device(err, as_np) if with_error else None)
+
+
 def inverse_frames(th: AdjustedTransform, tv: AdjustedTransform, coefs, height: int,
                    width: int):
     """Block-major coefficients -> (F, height, width) frames (padding clipped)."""

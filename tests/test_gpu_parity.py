@@ -508,3 +508,53 @@ def test_frames_interleaved_and_fallback(shape, name):
     assert rel_err(y.cpu().numpy(), want) < F32_TOL
     back = pipeline.inverse_frames(t, t, y, h, w)
     assert torch.equal(torch.round(back), dev(fr))
+
+
+def _exact_dst7_transform():
+    from paper_2505_23618_b200.design import AdjustmentMatrix, pattern_schedule_template
+    d7 = build_transform(TransformKind.DST7, 32).entries
+    dense = AdjustmentMatrix(SparsityPattern.dense(32), Side.POST, TransformKind.DCT2,
+                             TransformKind.DST7, pattern_schedule_template(SparsityPattern.dense(32)),
+                             d7 @ build_transform(TransformKind.DCT2, 32).entries.T)
+    return pipeline.make_adjusted_transform(dense)
+
+
+@pytest.mark.parametrize("shape", [(2, 70, 256), (1, 64, 128), (3, 40, 384), (2, 33, 96)])
+@pytest.mark.parametrize("name", ["sub8_post_dct2_dst7_n32", "band6_pre_dst3_dst7_n32"])
+def test_frames_exact_fused(shape, name):
+    """Config 5's comparison step in one call (fused tensor-core kernel when the
+    width holds 4-block super-tiles, the two-launch path otherwise): both outputs
+    against the oracle / numpy, the per-frame error sums against numpy on them."""
+    adj = matio.load_designed(name)
+    t = pipeline.make_adjusted_transform(adj)
+    te = _exact_dst7_transform()
+    f, h, w = shape
+    fr = np.random.default_rng(h * w).standard_normal(shape) * 30
+    ya, ye, err = pipeline.forward_frames_exact(t, t, te, te, dev(fr))
+    ty, tx = -(-h // 32), w // 32
+    blocks = _frame_tiles(fr, ty, tx)
+    ax = oaxis(adj)
+    assert rel_err(ya.cpu().numpy(), O.adjusted_2d(ax, ax, blocks)) < F32_TOL
+    me = pipeline.dense_matrix(te)
+    assert rel_err(ye.cpu().numpy(), me @ blocks @ me.T) < F32_TOL
+    a = ya.double().cpu().numpy().reshape(f, ty, tx, 32, 32)
+    e = ye.double().cpu().numpy().reshape(f, ty, tx, 32, 32)
+    full = h // 32
+    want = np.stack([((a - e) ** 2).sum(axis=(1, 2, 3, 4)), (e ** 2).sum(axis=(1, 2, 3, 4)),
+                     ((a - e)[:, :full] ** 2).sum(axis=(1, 2, 3, 4)),
+                     (e[:, :full] ** 2).sum(axis=(1, 2, 3, 4))], axis=1)
+    got = err.cpu().numpy()
+    assert got.shape == (f, 4)
+    assert np.allclose(got, want, rtol=1e-5, atol=1e-9 * want[:, 1:2].max())
+
+
+def test_frames_exact_without_error_matches():
+    """err = NULL takes the two-launch path; its outputs agree with the fused one."""
+    t = pipeline.make_adjusted_transform(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    te = _exact_dst7_transform()
+    fr = dev(np.random.default_rng(9).standard_normal((2, 64, 256)) * 30)
+    ya, ye, err = pipeline.forward_frames_exact(t, t, te, te, fr)
+    yb, yeb, none = pipeline.forward_frames_exact(t, t, te, te, fr, with_error=False)
+    assert none is None
+    assert rel_err(ya.cpu().numpy(), yb.double().cpu().numpy()) < F32_TOL
+    assert rel_err(ye.cpu().numpy(), yeb.double().cpu().numpy()) < F32_TOL

@@ -16,8 +16,14 @@ from paper_2505_23618_b200 import benchmark, pipeline  # noqa: E402
 from paper_2505_23618_b200.transforms import TransformKind, build_transform  # noqa: E402
 
 td = benchmark._dense_transform(build_transform(TransformKind.DST7, 32).entries)
-frames = len(sys.argv) > 1 and sys.argv[1] == "frames"
-if frames:  # config 5 shape: 64 frames of 2160 x 3840 (bottom tile row zero-filled)
+mode = sys.argv[1] if len(sys.argv) > 1 else "linear"
+if mode == "fused":  # config 5 comparison step: adjusted + exact in one kernel
+    from paper_2505_23618_b200 import matio
+    ta = pipeline.make_adjusted_transform(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    x = torch.randn(64, 2160, 3840, device="cuda")
+    for _ in range(3):
+        pipeline.forward_frames_exact(ta, ta, td, td, x)
+elif mode == "frames":  # config 5 shape: 64 frames of 2160 x 3840 (bottom tile row zero-filled)
     x = torch.randn(64, 2160, 3840, device="cuda")
     for _ in range(3):
         pipeline.forward_frames(td, td, x)
