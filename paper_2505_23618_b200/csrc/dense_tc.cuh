@@ -332,7 +332,7 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
         const int g = static_cast<int>(k % NGRP);
         const uint32_t par = static_cast<uint32_t>((k / NGRP) & 1);
         bool ok;
-        while (!(ok = mbar_test(&ready[g], par))) {
+        while (!(ok = mbar_test(&ready[g], par))) {  // spin: try_wait's suspend adds latency
           const int64_t tot = *total_k;
           if (tot >= 0 && k >= tot) break;
         }
