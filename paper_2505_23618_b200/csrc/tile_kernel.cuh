@@ -430,7 +430,8 @@ DA_DEV void group_sync(int grp) {
 template <typename T, int H, int W, int P, int RC, int CC, bool COL_FIRST, int IN_MODE,
           int OUT_MODE, int NG, int S, bool PAIR_ROW = false, bool PAIR_COL = false, int CH = 0,
           int NW = 1>
-__global__ void __launch_bounds__(NG * NW * 32)
+// CH bits 0-1: L2 hints; bits 4+: minimum resident CTAs per SM (register cap)
+__global__ void __launch_bounds__(NG * NW * 32, (CH >> 4) > 0 ? (CH >> 4) : 1)
     tile_kernel(const __grid_constant__ CUtensorMap in_map,
                 const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
                 const __grid_constant__ KParams<T, W, H, RC, CC> prm) {
