@@ -38,7 +38,10 @@ def to_device(x):
             t = t.to(torch.float64)
         if not t.is_cuda:
             return t.contiguous().to("cuda"), False
-        return t.contiguous(), False
+        t = t.contiguous()
+        if t.data_ptr() % 16:  # TMA needs 16-byte aligned bases (a view at an odd offset)
+            t = t.clone()
+        return t, False
     a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
     return torch.from_numpy(a).to("cuda"), True
 

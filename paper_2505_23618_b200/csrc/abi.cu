@@ -78,6 +78,8 @@ static EncodeFn get_encode() {
 int encode_tensor_map(CUtensorMap* map, int dtype, int rank, const uint64_t* dims,
                       const uint64_t* strides_bytes, const uint32_t* box, int box_row_bytes,
                       void* base) {
+  if (reinterpret_cast<uintptr_t>(base) & 15)
+    return fail(ST_ERR_VALUE, "data pointer %p is not 16-byte aligned (TMA requirement)", base);
   EncodeFn fn = get_encode();
   if (!fn) return fail(ST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t d[5], s[4];
@@ -414,6 +416,32 @@ static int check_dtype(int dtype) {
 }
 
 // ------------------------------------------------------------- 1-D batches
+// TMA coordinates are 32-bit: a LINEAR launch covers at most this many rows;
+// bigger batches run as several launches over consecutive sub-ranges
+// (DCTADJ_MAX_ROWS lowers the limit, for tests)
+static int64_t max_launch_rows() {
+  static const int64_t v = [] {
+    const char* s = std::getenv("DCTADJ_MAX_ROWS");
+    const long long r = s ? std::atoll(s) : 0;
+    return r > 0 ? static_cast<int64_t>(r) : (int64_t(1) << 30);
+  }();
+  return v;
+}
+
+// L.k->fn over `units` units of `unit_rows` rows / `unit_bytes` bytes each
+static int launch_linear_chunked(Launch& L, const void* x, void* y, int64_t units,
+                                 int64_t unit_rows, size_t unit_bytes) {
+  const int64_t per = std::max<int64_t>(1, max_launch_rows() / unit_rows);
+  for (int64_t u0 = 0; u0 < units; u0 += per) {
+    const int64_t nu = std::min(per, units - u0);
+    L.a.in = static_cast<const char*>(x) + static_cast<size_t>(u0) * unit_bytes;
+    L.a.out = static_cast<char*>(y) + static_cast<size_t>(u0) * unit_bytes;
+    L.a.rows = nu * unit_rows;
+    if (int rc = L.k->fn(L.a)) return rc;
+  }
+  return ST_OK;
+}
+
 static int run_1d(const AxisPlan& plan, const void* x, void* y, int64_t nvec, int dtype,
                   cudaStream_t st) {
   if (nvec < 0) return fail(ST_ERR_SHAPE, "negative batch size %lld", (long long)nvec);
@@ -424,10 +452,7 @@ static int run_1d(const AxisPlan& plan, const void* x, void* y, int64_t nvec, in
   if (rc == ST_ERR_UNSUPPORTED)
     return fail(rc, "no 1-D kernel for op 0x%x at n=%d dtype=%d", plan.code, plan.n, dtype);
   if (rc) return rc;
-  L.a.in = x;
-  L.a.out = y;
-  L.a.rows = nvec;
-  rc = L.k->fn(L.a);
+  rc = launch_linear_chunked(L, x, y, nvec, 1, static_cast<size_t>(plan.n) * dt_size(dtype));
   int rc2 = finish(L, st);
   return rc ? rc : rc2;
 }
@@ -631,8 +656,14 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
     a.stream = st;
     const int ty = (fh + H - 1) / H, tx = fw / W;
     const bool f4 = tx % 4 == 0;  // super-tiles never straddle a block row
-    if (in_mode == MODE_LINEAR && out_mode == MODE_LINEAR)
-      rc = launch_dense_tc<MODE_LINEAR, MODE_LINEAR>(a, nblk, 0, 0);
+    if (in_mode == MODE_LINEAR && out_mode == MODE_LINEAR) {
+      const int64_t per = std::max<int64_t>(4, max_launch_rows() / 32 / 4 * 4);  // whole super-tiles
+      for (int64_t b0 = 0; b0 < nblk && !rc; b0 += per) {
+        a.in = static_cast<const char*>(x) + static_cast<size_t>(b0) * 4096;
+        a.out = static_cast<char*>(y) + static_cast<size_t>(b0) * 4096;
+        rc = launch_dense_tc<MODE_LINEAR, MODE_LINEAR>(a, std::min(per, nblk - b0), 0, 0);
+      }
+    }
     else if (in_mode == MODE_FRAME)
       rc = f4 ? launch_dense_tc<MODE_FRAME4, MODE_LINEAR>(a, nblk, ty, tx)
               : launch_dense_tc<MODE_FRAME, MODE_LINEAR>(a, nblk, ty, tx);
@@ -675,13 +706,17 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
                   in_mode, out_mode);
   }
   if (rc) return rc;
-  L.a.in = x;
-  L.a.out = y;
-  L.a.rows = nblk * H;
   L.a.frames = frames;
   L.a.frame_h = fh;
   L.a.frame_w = fw;
-  rc = L.k->fn(L.a);
+  if (in_mode == MODE_LINEAR && out_mode == MODE_LINEAR) {
+    rc = launch_linear_chunked(L, x, y, nblk, H, static_cast<size_t>(H) * W * dt_size(dtype));
+  } else {
+    L.a.in = x;
+    L.a.out = y;
+    L.a.rows = nblk * H;
+    rc = L.k->fn(L.a);
+  }
   int rc2 = finish(L, st);
   return rc ? rc : rc2;
 }

@@ -558,3 +558,23 @@ def test_frames_exact_without_error_matches():
     assert none is None
     assert rel_err(ya.cpu().numpy(), yb.double().cpu().numpy()) < F32_TOL
     assert rel_err(ye.cpu().numpy(), yeb.double().cpu().numpy()) < F32_TOL
+
+
+def test_misaligned_views_and_pointers():
+    """A tensor view at a non-16-byte offset is copied by the Python layer (like
+    the reference's ascontiguousarray); a raw misaligned pointer through the
+    C-ABI is a ValueError, not a TMA fault."""
+    import ctypes
+    from paper_2505_23618_b200 import _lib
+    t = pipeline.make_adjusted_transform(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    base = torch.randn(5 * 32 + 1, 32, device="cuda")
+    view = base.view(-1)[1:1 + 4 * 32 * 32].view(4, 32, 32)  # 4-byte offset
+    assert view.data_ptr() % 16
+    got = pipeline.forward_adjusted_2d(t, t, view)
+    want = pipeline.forward_adjusted_2d(t, t, view.clone())
+    assert torch.equal(got, want)
+    ax, _keep = t.axis()
+    out = torch.empty(4, 32, 32, device="cuda")
+    with pytest.raises(ValueError):
+        _lib.call("dctadj_forward_2d", ctypes.byref(ax), ctypes.byref(ax), view.data_ptr(),
+                  out.data_ptr(), 4, _lib.F32, torch.cuda.current_stream().cuda_stream)
