@@ -539,6 +539,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         for _, fn in w.launches:
             fn()
     torch.cuda.synchronize()
+    # every output of a warm-up step is finite (the oracle gate samples blocks)
+    for name in ("y", "xr", "ye", "back"):
+        t = getattr(w, name, None)
+        if t is not None and not bool(torch.isfinite(t).all()):
+            raise SystemExit(f"non-finite values in {name} after the warm-up steps")
 
     # timed region: K steps back to back, CUDA events only at its two ends (an
     # event between launches would serialise the kernels' programmatic launch)

@@ -69,6 +69,8 @@ def c3_block(h: int, w: int, n: int, seed: int, device="cuda") -> torch.Tensor:
     16*sqrt(2) * L_v Z L_h^T with AR(1) rho = 0.9 (marginal only approx. Laplacian)."""
     g = torch.Generator(device=device).manual_seed(seed)
     u = torch.rand(n, h, w, device=device, generator=g) - 0.5
+    # rand() can return exactly 0 (u = -0.5): log1p(-1) = -inf; keep |u| < 0.5
+    u = u.clamp_(-0.5 + 2.0 ** -25, 0.5 - 2.0 ** -25)
     z = -(1.0 / math.sqrt(2.0)) * torch.sign(u) * torch.log1p(-2.0 * u.abs())
     lv = ar1_chol(h, 0.9, device, torch.float32)
     lh = ar1_chol(w, 0.9, device, torch.float32)
