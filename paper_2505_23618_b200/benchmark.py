@@ -142,7 +142,7 @@ def run_benchmark(pipelines=DEFAULT_PIPELINES, sizes=(32, 64), samples: int = 31
                     med, disp = _stats(_measure(fn, samples, warmup), coeffs)
                 dense_med[direction] = med
                 reports.append(BenchReport("dense", size, direction, med, 1.0, samples, disp, layout))
-                if layout == "2d" and size == 32 and dtype == "float32":
+                if layout == "2d" and dtype == "float32":
                     # the same product on the tensor cores (3xTF32 tcgen05, dense_tc.cuh)
                     med, disp = _stats(_measure(fn, samples, warmup), coeffs)
                     reports.append(BenchReport("dense_tc", size, direction, med,

@@ -16,6 +16,7 @@
 
 #include "../../include/dctadj.h"
 #include "dense_tc.cuh"
+#include "dense_tc64.cuh"
 #include "enc5.cuh"
 #include "launch.cuh"
 
@@ -213,7 +214,39 @@ static double mat_at(const dctadj_axis* ax, bool transpose, int r, int j) {
 }
 
 // The whole axis as one dense matrix (forward H = B*A or C*B; inverse H^T).
+static void composite_dense_uncached(const dctadj_axis* ax, bool inverse, std::vector<double>& out);
+
+// The composite (an O(n^3) host product plus n^2 cosines: ~150 us at n = 64) is
+// memoised by the axis contents, so repeated calls with the same transform cost
+// a comparison of the n x n input matrix.
+struct CompositeKey {
+  int n, base, adj, side, taps, order, inverse;
+  std::vector<double> mat;
+  bool operator==(const CompositeKey& o) const {
+    return n == o.n && base == o.base && adj == o.adj && side == o.side && taps == o.taps &&
+           order == o.order && inverse == o.inverse && mat == o.mat;
+  }
+};
 static void composite_dense(const dctadj_axis* ax, bool inverse, std::vector<double>& out) {
+  static std::mutex mu;
+  static std::vector<std::pair<CompositeKey, std::vector<double>>> memo;
+  CompositeKey key{ax->n, ax->base, ax->adj, ax->side, ax->taps, ax->order, inverse ? 1 : 0, {}};
+  if (ax->mat) key.mat.assign(ax->mat, ax->mat + static_cast<size_t>(ax->n) * ax->n);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : memo)
+      if (e.first == key) {
+        out = e.second;
+        return;
+      }
+  }
+  composite_dense_uncached(ax, inverse, out);
+  std::lock_guard<std::mutex> lk(mu);
+  if (memo.size() >= 32) memo.erase(memo.begin());
+  memo.emplace_back(std::move(key), out);
+}
+
+static void composite_dense_uncached(const dctadj_axis* ax, bool inverse, std::vector<double>& out) {
   const int n = ax->n;
   std::vector<double> b, a(static_cast<size_t>(n) * n, 0.0), h(static_cast<size_t>(n) * n, 0.0);
   base_matrix(ax->base, n, b);
@@ -624,6 +657,48 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   return ST_OK;
 }
 
+// 64x64 fp32 dense on the tensor cores (dense_tc64.cuh), LINEAR blocks
+static int launch_dense_tc64(const LaunchArgs& a, int64_t nblocks) {
+  constexpr int S = 3;  // 3 x 32 KB ring + 2 x 32 KB staging + 64 KB matrices: 224 KB
+  constexpr int NG = kTc64Groups;
+  Geom g{};
+  g.nblocks = nblocks;
+  g.ntiles = (nblocks + 1) / 2;
+  LaunchArgs la = a;
+  la.rows = nblocks * 64;
+  CUtensorMap in_map, out_map;
+  int rc = make_map<float, 64, 64, 2, MODE_LINEAR>(&in_map, a.in, la);
+  if (!rc) rc = make_map<float, 64, 64, 2, MODE_LINEAR>(&out_map, a.out, la);
+  if (rc) return rc;
+  DenseTcParams prm{static_cast<const float*>(a.dense_row), static_cast<const float*>(a.dense_col),
+                    nullptr, nullptr, nullptr, 0};
+  if ((rc = stream_sched_counter(a.stream, &prm.sched))) return rc;
+  auto kern = dense_tc64_kernel<S>;
+  const size_t smem = 1024 + S * 32768 + NG * 32768 + 65536 + (2 * S + 4 * NG) * 8 + (S + 1) * 8 + 16;
+  static int configured = 0;
+  if (!configured) {
+    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    int bps = 0;
+    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kTc64Threads, smem));
+    if (bps < 1) return fail(ST_ERR_CUDA, "64-point tensor-core kernel does not fit an SM");
+    configured = 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(g.ntiles, num_sms_cached())));
+  cfg.blockDim = dim3(kTc64Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm));
+  return ST_OK;
+}
+
 // ------------------------------------------------------------- 2-D / frames
 static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
                   int64_t nblk, int dtype, bool inverse, int in_mode, int out_mode,
@@ -640,6 +715,25 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
   if (!x || !y) return fail(ST_ERR_VALUE, "NULL data pointer");
   const int H = pv.n, W = ph.n;
   Launch L;
+  if (dtype == DT_F32 && H == 64 && W == 64 && ph.code == op_code(ST_DENSE) &&
+      pv.code == op_code(ST_DENSE) && dense_tc_enabled() && in_mode == MODE_LINEAR &&
+      out_mode == MODE_LINEAR) {
+    // 64x64 dense on the tensor cores (dense_tc64.cuh)
+    if ((rc = upload_dense(ph, dtype, st, &L.dense_row)) || (rc = upload_dense(pv, dtype, st, &L.dense_col)))
+      return rc;
+    LaunchArgs a;
+    a.dense_row = L.dense_row;
+    a.dense_col = L.dense_col;
+    a.stream = st;
+    const int64_t per = std::max<int64_t>(2, max_launch_rows() / 64 / 2 * 2);  // whole super-tiles
+    for (int64_t b0 = 0; b0 < nblk && !rc; b0 += per) {
+      a.in = static_cast<const char*>(x) + static_cast<size_t>(b0) * 16384;
+      a.out = static_cast<char*>(y) + static_cast<size_t>(b0) * 16384;
+      rc = launch_dense_tc64(a, std::min(per, nblk - b0));
+    }
+    int rc2 = finish(L, st);
+    return rc ? rc : rc2;
+  }
   if (dtype == DT_F32 && H == 32 && W == 32 && ph.code == op_code(ST_DENSE) &&
       pv.code == op_code(ST_DENSE) && dense_tc_enabled() && in_mode != MODE_GATHER) {
     // the dense comparison path on the tensor cores (3xTF32 tcgen05, dense_tc.cuh)

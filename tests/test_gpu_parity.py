@@ -578,3 +578,35 @@ def test_misaligned_views_and_pointers():
     with pytest.raises(ValueError):
         _lib.call("dctadj_forward_2d", ctypes.byref(ax), ctypes.byref(ax), view.data_ptr(),
                   out.data_ptr(), 4, _lib.F32, torch.cuda.current_stream().cuda_stream)
+
+
+def _dense_pair_n(n, seed_h, seed_v):
+    mk = lambda s: pipeline.make_adjusted_transform(  # noqa: E731
+        random_adjustment(SparsityPattern.dense(n), Side.POST, TransformKind.DCT2, s))
+    return mk(seed_h), mk(seed_v)
+
+
+@pytest.mark.parametrize("nblk", [1, 2, 3, 37, 1001])
+def test_dense_tc64_2d_ragged(nblk):
+    """64x64 fp32 dense on the tensor cores (dense_tc64.cuh): distinct row / column
+    matrices, odd block counts (half-empty 2-block super-tiles), oracle parity."""
+    th, tv = _dense_pair_n(64, 21, 22)
+    x = np.random.default_rng(nblk).standard_normal((nblk, 64, 64))
+    ah, av = oaxis(th.adjustment), oaxis(tv.adjustment)
+    y = pipeline.forward_adjusted_2d(th, tv, dev(x)).cpu().numpy()
+    assert rel_err(y, O.adjusted_2d(ah, av, x)) < F32_TOL
+    xr = pipeline.inverse_adjusted_2d(th, tv, dev(y)).cpu().numpy()
+    assert rel_err(xr, O.adjusted_2d(ah, av, y.astype(np.float64), inverse=True)) < F32_TOL
+
+
+def test_dense_tc64_repeat_and_streams():
+    th, tv = _dense_pair_n(64, 23, 24)
+    x = torch.randn(5000, 64, 64, device="cuda")
+    y0 = pipeline.forward_adjusted_2d(th, tv, x)
+    for _ in range(3):
+        assert torch.equal(pipeline.forward_adjusted_2d(th, tv, x), y0)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        y1 = pipeline.forward_adjusted_2d(th, tv, x)
+    s.synchronize()
+    assert torch.equal(y1, y0)

@@ -1,5 +1,5 @@
-"""Dense 32x32 fp32 2-D transform (tensor-core path unless DCTADJ_DENSE_TC=0),
-65,536 blocks, a few back-to-back launches (for ncu / timing)."""
+"""Dense 32x32 (or 64x64: argv[2]) fp32 2-D transform (tensor-core path unless
+DCTADJ_DENSE_TC=0), 64 M coefficients, a few back-to-back launches (ncu / timing)."""
 import sys
 from pathlib import Path
 
@@ -9,8 +9,9 @@ import torch  # noqa: E402
 from paper_2505_23618_b200 import benchmark, pipeline  # noqa: E402
 from paper_2505_23618_b200.transforms import TransformKind, build_transform  # noqa: E402
 
-td = benchmark._dense_transform(build_transform(TransformKind.DST7, 32).entries)
-x = torch.randn(65536, 32, 32, device="cuda")
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 32  # block size: 32 or 64
+td = benchmark._dense_transform(build_transform(TransformKind.DST7, n).entries)
+x = torch.randn(65536 * 1024 // (n * n), n, n, device="cuda")
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 for _ in range(3):
     y = pipeline.forward_adjusted_2d(td, td, x)
@@ -21,7 +22,7 @@ for _ in range(iters):
     y = pipeline.forward_adjusted_2d(td, td, x)
 e1.record()
 torch.cuda.synchronize()
-print(f"dense fwd {e0.elapsed_time(e1) / iters * 1e3:.1f} us per launch")
+print(f"dense {n}x{n} fwd {e0.elapsed_time(e1) / iters * 1e3:.1f} us per launch (HBM floor {x.numel() * 8 / 6553.6e3:.1f} us)")
 import time  # noqa: E402
 torch.cuda.synchronize()
 t0 = time.perf_counter()

@@ -15,8 +15,9 @@ out = ["# Table 1 on B200 -- throughput ratio vs the full-matrix transform", "",
        "1-D: 4,194,304 vectors per launch (the reference's layout); 2-D: 65,536 32x32 /",
        "16,384 64x64 blocks per launch, one fused kernel per transform.",
        "`dense` is the full-matrix FMA product on the CUDA cores (the paper's baseline, ratio",
-       "1.00); `dense_tc` is the same 32x32 fp32 product on the tensor cores (3xTF32 tcgen05,",
-       "csrc/dense_tc.cuh) and `multiple_vs_tc` the shared encoder against five of those.", "",
+       "1.00); `dense_tc` is the same fp32 product on the tensor cores (3xTF32 tcgen05,",
+       "csrc/dense_tc.cuh, dense_tc64.cuh) and `multiple_vs_tc` the shared encoder against",
+       "five of those (32x32).", "",
        "## 1-D batches", "", benchmark.report_table(reps, "1d"), "",
        "## 2-D blocks", "", benchmark.report_table(reps, "2d"), "",
        "## absolute throughput (G coefficients / s)", "",
