@@ -465,10 +465,12 @@ def _cpu_worker(args):
     return time.perf_counter() - t0
 
 
-def cpu_throughput(cfg_name: str, seconds: float = 8.0):
+def cpu_throughput(cfg_name: str, seconds: float = 8.0, pool=None, reps: int = 0):
     """Reference CPU path on this host's cores: the reference's compiled core
     (oracle/_ref, kind "reference") when built, else the C port (kind "port");
-    one process per core, each on its own block sample, single-threaded BLAS."""
+    one process per core, each on its own block sample, single-threaded BLAS.
+    `reps` > 0 fixes the passes per process (else sized to ~`seconds`); `pool`
+    reuses a caller's fork pool."""
     from multiprocessing import get_context
     from oracle import oracle as O
     if cfg_name not in UNIFORM:
@@ -479,10 +481,15 @@ def cpu_throughput(cfg_name: str, seconds: float = 8.0):
     nblk = 256 if n == 32 else 64
     per_pass = nblk * n * n * (2 if inverse else 1)
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    t1 = _cpu_worker((kind, cfg_name, nblk, 0, 1))
-    reps = max(1, int(seconds / max(t1, 1e-6)))
-    with get_context("fork").Pool(cores) as pool:
-        times = pool.map(_cpu_worker, [(kind, cfg_name, nblk, s, reps) for s in range(cores)])
+    if reps <= 0:
+        t1 = _cpu_worker((kind, cfg_name, nblk, 0, 1))
+        reps = max(1, int(seconds / max(t1, 1e-6)))
+    jobs = [(kind, cfg_name, nblk, s, reps) for s in range(cores)]
+    if pool is None:
+        with get_context("fork").Pool(cores) as own:
+            times = own.map(_cpu_worker, jobs)
+    else:
+        times = pool.map(_cpu_worker, jobs)
     value = cores * reps * per_pass / max(times)
     sample = (f"{cores} processes x {reps} passes x {nblk} blocks ({n}x{n}, "
               f"{'fwd+inv' if inverse else 'fwd'}) of the {cfg_name} workload")
@@ -490,21 +497,36 @@ def cpu_throughput(cfg_name: str, seconds: float = 8.0):
 
 
 def run_reference(args, rank: int, world: int):
+    """`--impl reference`: the reference's CPU path alone (rank 0; other ranks exit).
+    Each step is a bounded sample of the workload on every host core; the sample
+    is sized so the whole --warmup + --steps run takes about `--ref-seconds`."""
     if rank != 0:
         return
+    from multiprocessing import get_context
+    from oracle import oracle as O
     cfg = args.config if args.config in UNIFORM else "c2"
-    wl, _, _, dt, _, _, _ = UNIFORM[cfg]
+    wl, _, n, dt, _, _, _ = UNIFORM[cfg]
+    nsteps = args.warmup + args.steps
+    per_step = min(2.0, max(0.02, args.ref_seconds / nsteps))
+    kind = "reference" if O.ref_fastcore() is not None else "port"
+    nblk = 256 if n == 32 else 64
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    t1 = _cpu_worker((kind, cfg, nblk, 0, 1))
+    reps = max(1, int(per_step / max(t1, 1e-6)))
     per = []
     res = None
-    for i in range(args.warmup + args.steps):
-        r = cpu_throughput(cfg, seconds=2.0)
-        if i >= args.warmup:
-            per.append(r["value"])
-            res = r
+    with get_context("fork").Pool(O.threads_available()) as pool:
+        for i in range(nsteps):
+            r = cpu_throughput(cfg, pool=pool, reps=reps)
+            if i >= args.warmup:
+                per.append(r["value"])
+                res = r
     value = float(np.median(per))
     res["value"] = value
+    per_step_coefs = O.threads_available() * reps * nblk * n * n * (2 if UNIFORM[cfg][6] else 1)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": per_step_coefs / value * 1e3,
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
             "impl": "reference", "config": {"workload": wl, "sample_per_step": res["sample"]},
             "cpu_baseline": res,
@@ -684,6 +706,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-seconds", type=float, default=120.0,
+                    help="--impl reference: total CPU time budget over warmup + steps")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
