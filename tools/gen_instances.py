@@ -69,7 +69,13 @@ def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False
         if givens or col_first:
             # 64-point vectors: two warps per tile, scalar lanes, 12 warps/SM
             # (the packed 64-column pass needs ~200 registers; measured faster)
-            return p, 6, 2, ("NW2",)
+            return p, 6, 2, ("NW", 2, 0)
+    if two_d and dtype == "double" and (h, w) == (32, 32):
+        # fp64 32x32 (config 1): two warps per 2-block super-tile, two stages, and a
+        # 170-register cap (launch bounds: 6 CTAs/SM) -> 12 warps/SM, no spills.
+        # Measured 14.3 us vs 16.9 us per 4,096-block forward (4 x 1 warp, 3 stages,
+        # 255 registers, 8 warps/SM); profiles/r01_tuning.md
+        return 2, 1, 2, ("NW", 2, 0x60)
     if stage <= 2048:
         ng, s = 8, 4
     elif stage <= 4096:
@@ -140,7 +146,11 @@ def pair_flags(dt, h, w, p, rc, cc):
 EXPERIMENT = {
     ("double", 32, 32): [(1, 8, 2, False, False, 0, 1), (1, 2, 4, False, False, 0, 1),
                          (2, 2, 2, False, False, 0, 2), (2, 3, 2, False, False, 0, 2),
-                         (2, 1, 4, False, False, 0, 2), (1, 12, 2, False, False, 0, 1)],
+                         (2, 1, 4, False, False, 0, 2), (1, 12, 2, False, False, 0, 1),
+                         (2, 1, 3, False, False, 0, 2), (2, 1, 2, False, False, 0x60, 2),
+                         (2, 1, 3, False, False, 0x50, 2), (4, 1, 3, False, False, 0, 4),
+                         (4, 1, 2, False, False, 0x30, 4), (2, 1, 4, False, False, 0x40, 2),
+                         (1, 6, 2, False, False, 0, 1), (2, 1, 5, False, False, 0, 2)],
     ("float", 32, 32): [(4, 2, 3, True, True, 0), (2, 4, 4, True, True, 0), (4, 2, 3, False, True, 0),
                (2, 4, 4, False, True, 0)],
     ("float", 64, 64): [(1, 6, 2, False, False, 0, 2), (1, 4, 3, False, False, 0, 2),
@@ -217,10 +227,10 @@ def instances():
     for inst in out:
         dt, h, w, p, rc, cc, cf, im, om, ng, s_, pr = inst
         _, pc = pair_flags(dt, h, w, p, rc, cc)
-        if pr == ("NW2",):  # two warps per tile, scalar lanes
-            final.append(inst[:11] + (False, False, 0, 0, 2))
-            continue
-        final.append(inst[:11] + (pr and cc != ID, pc, 0, 0))
+        if isinstance(pr, tuple) and pr[0] == "NW":  # NW warps per tile, scalar lanes, CH bits
+            final.append(inst[:11] + (False, False, 0, pr[2], pr[1]))
+        else:
+            final.append(inst[:11] + (pr and cc != ID, pc, 0, 0))
         if (im, om) == (2, 2):
             binv = cf and (rc >> 8) in (4, 6) and (rc & 15) != SUB and ((rc >> 4) & 15) in (BAND, GIVENS)
             exps = GATHER_BINV_EXPERIMENT if binv else GATHER_EXPERIMENT
@@ -264,7 +274,11 @@ def main():
     ROOT.mkdir(parents=True, exist_ok=True)
     insts = instances()
     shards = [[] for _ in range(NSHARDS)]
+    seen = set()
     for i, inst in enumerate(insts):
+        if _targs(inst) in seen:  # a tuning variant equal to a default: one definition
+            continue
+        seen.add(_targs(inst))
         shards[i % NSHARDS].append(inst)
     reg = ["// Generated by tools/gen_instances.py -- do not edit.",
            f"// {len(insts)} tile_kernel instantiations."]
@@ -277,10 +291,13 @@ def main():
         _write_if_changed(ROOT / f"inst_{k:02d}.cu", "\n".join(lines))
     decl = []
     rows = []
+    declared = set()
     for inst in insts:
         dt, h, w, p, rc, cc, cf, im, om, ng, s, pr, pc, var, ch = inst[:15]
         targs = _targs(inst)
-        decl.append(f"extern template int launch_tile<{targs}>(const LaunchArgs&);")
+        if targs not in declared:
+            declared.add(targs)
+            decl.append(f"extern template int launch_tile<{targs}>(const LaunchArgs&);")
         rows.append(f"  {{{DTYPES[dt]}, {h}, {w}, {rc}, {cc}, {int(cf)}, {im}, {om}, {var}, "
                     f"&launch_tile<{targs}>}},")
     reg += decl + ["", "static const KernelEntry kRegistry[] = {"] + rows + ["};", ""]
