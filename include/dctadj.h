@@ -117,6 +117,14 @@ int dctadj_forward_2d_host(const dctadj_axis* h, const dctadj_axis* v, const voi
                            void* y_host, int64_t nblk, int32_t dtype, int32_t device);
 int dctadj_inverse_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* y_host,
                            void* x_host, int64_t nblk, int32_t dtype, int32_t device);
+/* Round trip on host buffers (config 2's step): y_host = forward(x_host) and
+ * xr_host = inverse(y_host), the inverse run on the device-resident
+ * coefficients of each chunk (one H2D, two D2H per chunk).  Same results as
+ * dctadj_forward_2d_host followed by dctadj_inverse_2d_host.  Composes the
+ * reference's forward_adjusted / inverse_adjusted (pipeline.py:176-191). */
+int dctadj_roundtrip_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x_host,
+                             void* y_host, void* xr_host, int64_t nblk, int32_t dtype,
+                             int32_t device);
 
 /* ---- frame tiling: frames (nframes, height, width) <-> block-major
  * coefficients (nframes * ceil(height/H) * (width/W), H, W).  Rows past

@@ -69,6 +69,7 @@ SIGNATURES = {
     "dctadj_inverse_2d": [_AP, _AP, _P, _P, _I64, _I32, _P],
     "dctadj_forward_2d_host": [_AP, _AP, _P, _P, _I64, _I32, _I32],
     "dctadj_inverse_2d_host": [_AP, _AP, _P, _P, _I64, _I32, _I32],
+    "dctadj_roundtrip_2d_host": [_AP, _AP, _P, _P, _P, _I64, _I32, _I32],
     "dctadj_forward_frames": [_AP, _AP, _P, _P, _I32, _I32, _I32, _I32, _P],
     "dctadj_inverse_frames": [_AP, _AP, _P, _P, _I32, _I32, _I32, _I32, _P],
     "dctadj_forward_frames_exact": [_AP, _AP, _AP, _AP, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P],

@@ -843,8 +843,11 @@ static size_t host_chunk_bytes() {
   return v;
 }
 
+// xrh != NULL (round trip, config 2): each chunk also runs the inverse on the
+// device-resident coefficients and copies the reconstruction back, so the
+// coefficients cross PCIe once (D2H) instead of three times.
 static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* xh, void* yh,
-                       int64_t nblk, int dtype, bool inverse, int device) {
+                       int64_t nblk, int dtype, bool inverse, int device, void* xrh = nullptr) {
   int rc = check_dtype(dtype);
   if (rc) return rc;
   if ((rc = validate_axis(h)) != ST_OK || (rc = validate_axis(v)) != ST_OK) return rc;
@@ -891,8 +894,18 @@ static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x
                     0, 0, hp.st[k]);
     if (status) break;
     if (cudaMemcpyAsync(static_cast<char*>(yh) + off, hp.dout[k], bytes, cudaMemcpyDeviceToHost,
-                        hp.st[k]) != cudaSuccess)
+                        hp.st[k]) != cudaSuccess) {
       status = fail(ST_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    if (xrh) {  // inverse of the chunk's coefficients into the (consumed) input buffer
+      status = run_2d(h, v, hp.dout[k], hp.din[k], nb, dtype, true, MODE_LINEAR, MODE_LINEAR, 0, 0,
+                      0, hp.st[k]);
+      if (status) break;
+      if (cudaMemcpyAsync(static_cast<char*>(xrh) + off, hp.din[k], bytes, cudaMemcpyDeviceToHost,
+                          hp.st[k]) != cudaSuccess)
+        status = fail(ST_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
+    }
   }
   for (int i = 0; i < HostPipe::NSTREAM; ++i) {
     cudaError_t e = cudaStreamSynchronize(hp.st[i]);
@@ -1372,6 +1385,12 @@ int dctadj_forward_2d_host(const dctadj_axis* h, const dctadj_axis* v, const voi
 int dctadj_inverse_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* y_host,
                            void* x_host, int64_t nblk, int32_t dtype, int32_t device) {
   return run_2d_host(h, v, y_host, x_host, nblk, dtype, true, device);
+}
+int dctadj_roundtrip_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x_host,
+                             void* y_host, void* xr_host, int64_t nblk, int32_t dtype,
+                             int32_t device) {
+  if (!xr_host && nblk > 0) return fail(ST_ERR_VALUE, "NULL data pointer");
+  return run_2d_host(h, v, x_host, y_host, nblk, dtype, false, device, xr_host);
 }
 
 int dctadj_forward_frames(const dctadj_axis* h, const dctadj_axis* v, const void* frames,

@@ -15,6 +15,7 @@ round trip) behind the C-ABI.  New entries:
                                               pipeline.py:236-239), one kernel
   forward_frames / inverse_frames             whole frames tiled into blocks
   forward_adjusted_2d_host / ..._host         host buffers, pipelined copies
+  roundtrip_adjusted_2d_host                  forward + inverse on host buffers, one pass
   MixedBatch / mixed_forward / mixed_inverse  packed mixed-shape batches (config 3)
 Extension: base DCT-3 is accepted (the DCT-8 pre-adjustment, SURVEY.md App. A
 D3, built with design.flip_pre_adjustment); the reference raises
@@ -238,6 +239,17 @@ def inverse_adjusted_2d(th: AdjustedTransform, tv: AdjustedTransform, y):
     return _run_2d("dctadj_inverse_2d", th, tv, y)
 
 
+def _host_out(arr: np.ndarray, out):
+    """A fresh output like `arr`, or the caller's array checked to be a writable
+    C-contiguous ndarray of the same shape and dtype (the library writes it raw)."""
+    if out is None:
+        return np.empty_like(arr)
+    if not isinstance(out, np.ndarray) or out.shape != arr.shape or out.dtype != arr.dtype \
+            or not out.flags.c_contiguous or not out.flags.writeable:
+        raise ShapeError(f"out must be a writable C-contiguous {arr.dtype} array of shape {arr.shape}")
+    return out
+
+
 def _run_2d_host(fn: str, th: AdjustedTransform, tv: AdjustedTransform, x, out=None):
     arr = np.asarray(x)
     if arr.dtype not in (np.float32, np.float64):
@@ -245,7 +257,7 @@ def _run_2d_host(fn: str, th: AdjustedTransform, tv: AdjustedTransform, x, out=N
     arr = np.ascontiguousarray(arr)
     if arr.ndim != 3 or arr.shape[1:] != (tv.size, th.size):
         raise ShapeError(f"expected (nblk, {tv.size}, {th.size}) blocks, got {arr.shape}")
-    y = np.empty_like(arr) if out is None else out
+    y = _host_out(arr, out)
     (axh, _kh), (axv, _kv) = th.axis(), tv.axis()
     _device.require_cuda()
     _lib.call(fn, ctypes.byref(axh), ctypes.byref(axv), arr.ctypes.data, y.ctypes.data,
@@ -262,6 +274,27 @@ def forward_adjusted_2d_host(th, tv, x, out=None):
 
 def inverse_adjusted_2d_host(th, tv, y, out=None):
     return _run_2d_host("dctadj_inverse_2d_host", th, tv, y, out)
+
+
+def roundtrip_adjusted_2d_host(th, tv, x, out=None, out_inv=None):
+    """(forward_adjusted_2d(x), inverse_adjusted_2d(of that)) on host arrays in one
+    pipelined pass: the coefficients stay on the device for the inverse and
+    cross PCIe once.  Returns (y, xr)."""
+    arr = np.asarray(x)
+    if arr.dtype not in (np.float32, np.float64):
+        arr = arr.astype(np.float64)
+    arr = np.ascontiguousarray(arr)
+    if arr.ndim != 3 or arr.shape[1:] != (tv.size, th.size):
+        raise ShapeError(f"expected (nblk, {tv.size}, {th.size}) blocks, got {arr.shape}")
+    y = _host_out(arr, out)
+    xr = _host_out(arr, out_inv)
+    (axh, _kh), (axv, _kv) = th.axis(), tv.axis()
+    _device.require_cuda()
+    _lib.call("dctadj_roundtrip_2d_host", ctypes.byref(axh), ctypes.byref(axv), arr.ctypes.data,
+              y.ctypes.data, xr.ctypes.data, arr.shape[0],
+              _lib.F32 if arr.dtype == np.float32 else _lib.F64,
+              _device.torch.cuda.current_device())
+    return y, xr
 
 
 # ---------------------------------------------------------------- frames

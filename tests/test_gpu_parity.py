@@ -246,6 +246,18 @@ def test_c2_host_entry(golden):
     assert rel_err(y, golden["c2/y"]) < F32_TOL
     xr = pipeline.inverse_adjusted_2d_host(t, t, y)
     assert np.array_equal(np.rint(xr), x)
+    # round trip in one pipelined pass: identical to the two calls, bit for bit,
+    # also across several pipeline chunks (1 MB chunks -> 16+ chunks here)
+    y2, xr2 = pipeline.roundtrip_adjusted_2d_host(t, t, x)
+    assert np.array_equal(y2, y) and np.array_equal(xr2, xr)
+    big = np.ascontiguousarray(np.tile(x, (max(1, 4096 // x.shape[0]), 1, 1)))
+    yb, xb = pipeline.roundtrip_adjusted_2d_host(t, t, big)
+    assert np.array_equal(yb, pipeline.forward_adjusted_2d_host(t, t, big))
+    assert np.array_equal(np.rint(xb), big)
+    for fp64 in (False, True):
+        xin = big.astype(np.float64) if fp64 else big
+        yb, xb = pipeline.roundtrip_adjusted_2d_host(t, t, xin)
+        assert rel_err(xb, xin) < (F64_TOL if fp64 else F32_TOL)
 
 
 @pytest.mark.parametrize("tag", ["dst7_pre", "dct8_pre", "dst7_post", "dct8_post"])

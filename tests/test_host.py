@@ -174,6 +174,29 @@ def test_validation_errors_without_device():
                                              1, 64, 40, 0, None))
     # empty batches are a no-op success
     _lib.check(lib.dctadj_forward_1d(ctypes.byref(ax), None, None, 0, 0, None))
+    _lib.check(lib.dctadj_roundtrip_2d_host(ctypes.byref(ax), ctypes.byref(ax), None, None, None,
+                                            0, 0, 0))
+    with pytest.raises(ValueError):
+        _lib.check(lib.dctadj_roundtrip_2d_host(ctypes.byref(ax), ctypes.byref(ax), None, None,
+                                                None, 4, 0, 0))
+
+
+def test_host_entry_rejects_bad_out_arrays():
+    """The host entries write caller arrays raw: shape, dtype, contiguity and
+    writability are checked before any device work."""
+    from paper_2505_23618_b200 import pipeline
+    from paper_2505_23618_b200.design import dct8_adjustment_from_dst7
+    t = pipeline.make_adjusted_transform(
+        dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32")))
+    x = np.zeros((4, 32, 32), np.float32)
+    ro = np.zeros_like(x)
+    ro.flags.writeable = False
+    for bad in (np.zeros((3, 32, 32), np.float32), np.zeros_like(x, dtype=np.float64),
+                np.zeros((4, 32, 64), np.float32)[:, :, ::2], ro):
+        with pytest.raises(errors.ShapeError):
+            pipeline.forward_adjusted_2d_host(t, t, x, out=bad)
+        with pytest.raises(errors.ShapeError):
+            pipeline.roundtrip_adjusted_2d_host(t, t, x, out_inv=bad)
 
 
 # ---------------------------------------------------------------- partitioning
