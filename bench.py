@@ -153,10 +153,12 @@ def _peaks():
     return 6650.0, "fallback"
 
 
-def _traffic(workload: str):
+def _traffic(workload: str, launch: str):
+    """ncu dram bytes (read + write) of one `launch` of `workload`, from
+    profiles/ncu_traffic.json (keys "<workload>/<launch>")."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
-        return json.loads(p.read_text()).get(workload)
+        return json.loads(p.read_text()).get(f"{workload}/{launch}")
     return None
 
 
@@ -192,7 +194,7 @@ class Workload:
 
 
 class Uniform(Workload):
-    def __init__(self, name: str, rank: int):
+    def __init__(self, name: str, rank: int, fused_roundtrip: bool = False):
         import torch
         from paper_2505_23618_b200 import _lib, pipeline, workloads
         wl, nblk, n, dt, make, inputs, inverse = UNIFORM[name]
@@ -220,7 +222,16 @@ class Uniform(Workload):
         def inv():
             _lib.check(lib.dctadj_inverse_2d(ref, ref, self.y.data_ptr(), self.xr.data_ptr(), nblk, dtc, st))
 
-        self.launches = [("forward_2d", fwd)] + ([("inverse_2d", inv)] if inverse else [])
+        def rt():  # forward + inverse in one kernel: x read once, y and x' written once
+            _lib.check(lib.dctadj_roundtrip_2d(ref, ref, self.x.data_ptr(), self.y.data_ptr(),
+                                               self.xr.data_ptr(), nblk, dtc, st))
+
+        self.unfused = [("forward_2d", fwd)] + ([("inverse_2d", inv)] if inverse else [])
+        self.launches = self.unfused
+        if fused_roundtrip and inverse:
+            self.launches = [("roundtrip_2d", rt)]
+            self.bytes_first_launch = 3 * coef * es
+            self.kernel_name = "roundtrip_kernel"
         self._lib, self._dtc, self._st, self._ref = lib, dtc, st, ref
         # e2e: the same step through the host-buffer entries (pinned arrays)
         self.xh = self.x.cpu().pin_memory().numpy()
@@ -553,7 +564,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.config in UNIFORM:
-        w = Uniform(args.config, rank)
+        w = Uniform(args.config, rank, fused_roundtrip=args.config == "c2" and not args.unfused)
     elif args.config.startswith("c3"):
         w = Mixed(args.config.split("_")[1], rank)
     else:
@@ -610,6 +621,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         b.record(stream)
         torch.cuda.synchronize()
         per_launch_ms.append(a.elapsed_time(b) / reps)
+
+    unfused = None
+    if getattr(w, "unfused", None) is not None and w.unfused is not w.launches:
+        ums = []
+        for _, fn in w.unfused:
+            fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ums.append(a.elapsed_time(b) / reps)
+        unfused = {"value": w.coef_per_step / (sum(ums) / 1e3),
+                   "per_launch_ms": dict(zip([n for n, _ in w.unfused], ums)),
+                   "note": "the same step as two kernels (forward_2d, inverse_2d), x and y each "
+                           "crossing HBM twice (16 B per coefficient pair instead of 12)"}
 
     # dispersion: per-step CUDA events over up to 50 further steps (median, IQR)
     nsamp = min(args.steps, 50)
@@ -675,6 +704,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     config.update(w.extra)
     if rot is not None:
         config["l2_rotating_buffers"] = rot
+    if unfused is not None:
+        config["schedule"] = "fused round trip: one kernel per step (dctadj_roundtrip_2d)"
+        config["unfused_two_kernels"] = unfused
     if approx is not None:
         config["approx_error_vs_exact_dst7_all_tiles"] = approx[0] / approx[1]
         config["approx_error_vs_exact_dst7_unpadded_tile_rows"] = approx[2] / approx[3]
@@ -685,7 +717,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "data": "synthetic (seeded residual fields per BASELINE.json configs, SURVEY.md App. A D12)",
         "config": config,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _traffic(w.workload),
+                     "frac": achieved / peak, "traffic": _traffic(w.workload, w.launches[0][0]),
                      "peak_source": peak_src,
                      "kernel": f"{w.kernel_name} ({w.launches[0][0]})",
                      "algorithmic_bytes_per_launch": w.bytes_first_launch,
@@ -715,6 +747,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=CONFIGS)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--unfused", action="store_true",
+                    help="c2: time forward and inverse as two kernels (x, y each cross HBM twice)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=120.0,
                     help="--impl reference: total CPU time budget over warmup + steps")

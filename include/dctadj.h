@@ -109,6 +109,14 @@ int dctadj_forward_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x,
                       int64_t nblk, int32_t dtype, void* stream);
 int dctadj_inverse_2d(const dctadj_axis* h, const dctadj_axis* v, const void* y, void* x,
                       int64_t nblk, int32_t dtype, void* stream);
+/* Round trip (config 2's step): y = forward(x) and xr = inverse(y) in one
+ * pass over HBM (x read once, y and xr written once: 12 B per coefficient pair
+ * in fp32 instead of 16 B).  Results are bit-identical to dctadj_forward_2d
+ * followed by dctadj_inverse_2d; op pairs without a fused kernel run as exactly
+ * those two calls.  xr may alias x; y must not alias xr.  Composes the
+ * reference's forward_adjusted / inverse_adjusted (pipeline.py:176-191). */
+int dctadj_roundtrip_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
+                        void* xr, int64_t nblk, int32_t dtype, void* stream);
 
 /* Host-buffer variants: x_host/y_host are host arrays (pinned for full speed);
  * copies, kernels and read-back are pipelined over chunks on internal streams.

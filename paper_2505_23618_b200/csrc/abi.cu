@@ -19,6 +19,7 @@
 #include "dense_tc64.cuh"
 #include "enc5.cuh"
 #include "launch.cuh"
+#include "roundtrip.cuh"
 
 namespace dctadj {
 
@@ -815,6 +816,71 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
   return rc ? rc : rc2;
 }
 
+// ------------------------------------------------------------- round trip
+// y = forward(x), xr = inverse(y) as ONE fused kernel (roundtrip.cuh) when one
+// is built for these ops, else the two tile kernels back to back (identical
+// results).  xr may alias x; y may not alias xr.  DCTADJ_RT_VARIANT=k picks a
+// tuning variant, DCTADJ_RT_UNFUSED=1 forces the two-kernel path.
+static int rt_variant() {
+  static int v = [] {
+    const char* s = std::getenv("DCTADJ_RT_VARIANT");
+    return s ? std::atoi(s) : 0;
+  }();
+  return v;
+}
+static bool rt_unfused() {
+  static bool v = [] {
+    const char* s = std::getenv("DCTADJ_RT_UNFUSED");
+    return s && s[0] == '1';
+  }();
+  return v;
+}
+
+static int run_roundtrip(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
+                         void* xr, int64_t nblk, int dtype, cudaStream_t st) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  AxisPlan fh, fv, ih, iv;
+  if ((rc = plan_axis(h, false, false, &fh)) || (rc = plan_axis(v, false, false, &fv)) ||
+      (rc = plan_axis(h, true, false, &ih)) || (rc = plan_axis(v, true, false, &iv)))
+    return rc;
+  if (nblk < 0) return fail(ST_ERR_SHAPE, "negative block count %lld", (long long)nblk);
+  if (nblk == 0) return ST_OK;
+  if (!x || !y || !xr) return fail(ST_ERR_VALUE, "NULL data pointer");
+  if (y == xr) return fail(ST_ERR_VALUE, "coefficients and reconstruction must not alias");
+  const int H = fv.n, W = fh.n;
+  const RtEntry* e = rt_unfused() ? nullptr
+                                  : find_roundtrip(dtype, H, W, fh.code, fv.code, ih.code, iv.code,
+                                                   rt_variant());
+  if (trace_on())
+    std::fprintf(stderr, "[dctadj] roundtrip dtype=%d %dx%d ops 0x%x/0x%x/0x%x/0x%x: %s\n", dtype, H,
+                 W, fh.code, fv.code, ih.code, iv.code, e ? "fused" : "two kernels");
+  if (!e) {
+    rc = run_2d(h, v, x, y, nblk, dtype, false, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, st);
+    if (!rc) rc = run_2d(h, v, y, xr, nblk, dtype, true, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, st);
+    return rc;
+  }
+  const std::vector<unsigned char> c0 = to_dtype(fh.coef, dtype), c1 = to_dtype(fv.coef, dtype),
+                                   c2 = to_dtype(ih.coef, dtype), c3 = to_dtype(iv.coef, dtype);
+  RtArgs a;
+  a.coef[0] = c0.data();
+  a.coef[1] = c1.data();
+  a.coef[2] = c2.data();
+  a.coef[3] = c3.data();
+  a.stream = st;
+  const size_t bb = static_cast<size_t>(H) * W * dt_size(dtype);
+  const int64_t per = std::max<int64_t>(1, max_launch_rows() / H);  // 32-bit TMA row range
+  for (int64_t b0 = 0; b0 < nblk && !rc; b0 += per) {
+    const int64_t nb = std::min(per, nblk - b0);
+    a.in = static_cast<const char*>(x) + static_cast<size_t>(b0) * bb;
+    a.y = static_cast<char*>(y) + static_cast<size_t>(b0) * bb;
+    a.xr = static_cast<char*>(xr) + static_cast<size_t>(b0) * bb;
+    a.rows = nb * H;
+    rc = e->fn(a);
+  }
+  return rc;
+}
+
 // Host-buffer pipeline: chunks of blocks cycle through NSTREAM streams, each
 // with its own device in/out buffers: H2D(c) overlaps kernel(c-1) and D2H(c-2)
 // (PCIe is full duplex).  Streams and staging buffers persist per device
@@ -890,18 +956,16 @@ static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x
       status = fail(ST_ERR_CUDA, "H2D copy: %s", cudaGetErrorString(cudaGetLastError()));
       break;
     }
-    status = run_2d(h, v, hp.din[k], hp.dout[k], nb, dtype, inverse, MODE_LINEAR, MODE_LINEAR, 0,
-                    0, 0, hp.st[k]);
+    status = xrh ? run_roundtrip(h, v, hp.din[k], hp.dout[k], hp.din[k], nb, dtype, hp.st[k])
+                 : run_2d(h, v, hp.din[k], hp.dout[k], nb, dtype, inverse, MODE_LINEAR,
+                          MODE_LINEAR, 0, 0, 0, hp.st[k]);
     if (status) break;
     if (cudaMemcpyAsync(static_cast<char*>(yh) + off, hp.dout[k], bytes, cudaMemcpyDeviceToHost,
                         hp.st[k]) != cudaSuccess) {
       status = fail(ST_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
       break;
     }
-    if (xrh) {  // inverse of the chunk's coefficients into the (consumed) input buffer
-      status = run_2d(h, v, hp.dout[k], hp.din[k], nb, dtype, true, MODE_LINEAR, MODE_LINEAR, 0, 0,
-                      0, hp.st[k]);
-      if (status) break;
+    if (xrh) {  // reconstruction of the chunk: written over its consumed input
       if (cudaMemcpyAsync(static_cast<char*>(xrh) + off, hp.din[k], bytes, cudaMemcpyDeviceToHost,
                           hp.st[k]) != cudaSuccess)
         status = fail(ST_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(cudaGetLastError()));
@@ -1376,6 +1440,10 @@ int dctadj_forward_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x,
 int dctadj_inverse_2d(const dctadj_axis* h, const dctadj_axis* v, const void* y, void* x,
                       int64_t nblk, int32_t dtype, void* stream) {
   return run_2d(h, v, y, x, nblk, dtype, true, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, S(stream));
+}
+int dctadj_roundtrip_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
+                        void* xr, int64_t nblk, int32_t dtype, void* stream) {
+  return run_roundtrip(h, v, x, y, xr, nblk, dtype, S(stream));
 }
 
 int dctadj_forward_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x_host,

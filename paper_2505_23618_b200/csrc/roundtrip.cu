@@ -1,0 +1,123 @@
+// roundtrip.cu -- launcher and instantiations of the fused forward + inverse
+// kernel (roundtrip.cuh).  Op pairs without an instantiation here run as the
+// two separate tile kernels (abi.cu), with identical results.
+#include "launch.cuh"
+#include "roundtrip.cuh"
+
+namespace dctadj {
+
+template <typename T, int H, int W, int P, int RCF, int CCF, int RCI, int CCI, int NG, int S,
+          bool PRF, bool PC, bool PRI, int MINB, bool YSTG>
+int launch_roundtrip(const RtArgs& a) {
+  using L = TileLayout<T, H, W, P>;
+  using Prm = RtParams<T, W, H, RCF, CCF, RCI, CCI>;
+  Geom g{};
+  g.ntiles = (a.rows + L::PH - 1) / L::PH;
+  g.nblocks = g.ntiles * P;
+  if (g.ntiles == 0) return ST_OK;
+  LaunchArgs la;
+  la.rows = a.rows;
+  CUtensorMap in_map, y_map, xr_map;
+  int rc = make_map<T, H, W, P, MODE_LINEAR>(&in_map, a.in, la);
+  if (!rc) rc = make_map<T, H, W, P, MODE_LINEAR>(&y_map, a.y, la);
+  if (!rc) rc = make_map<T, H, W, P, MODE_LINEAR>(&xr_map, a.xr, la);
+  if (rc) return rc;
+  Prm prm;
+  std::memset(&prm, 0, sizeof(prm));
+  if (AxisOp<T, W, RCF>::NCOEF > 0)
+    std::memcpy(prm.f.row.c, a.coef[0], sizeof(T) * AxisOp<T, W, RCF>::NCOEF);
+  if (AxisOp<T, H, CCF>::NCOEF > 0)
+    std::memcpy(prm.f.col.c, a.coef[1], sizeof(T) * AxisOp<T, H, CCF>::NCOEF);
+  if (AxisOp<T, W, RCI>::NCOEF > 0)
+    std::memcpy(prm.i.row.c, a.coef[2], sizeof(T) * AxisOp<T, W, RCI>::NCOEF);
+  if (AxisOp<T, H, CCI>::NCOEF > 0)
+    std::memcpy(prm.i.col.c, a.coef[3], sizeof(T) * AxisOp<T, H, CCI>::NCOEF);
+  prm.y = static_cast<T*>(a.y);
+  prm.nblk = a.rows / H;
+
+  auto kern = roundtrip_kernel<T, H, W, P, RCF, CCF, RCI, CCI, NG, S, PRF, PC, PRI, MINB, YSTG>;
+  const size_t smem = 1024 + static_cast<size_t>(NG) * (YSTG ? S : S + 1) * L::STAGEB + NG * S * 8;
+  static int blocks_per_sm = 0;  // per instantiation
+  if (!blocks_per_sm) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    int nb = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NG * 32, smem);
+    if (e != cudaSuccess || nb < 1) {
+      set_last_error("roundtrip_kernel setup: %s (%d blocks/SM)", cudaGetErrorString(e), nb);
+      return ST_ERR_CUDA;
+    }
+    blocks_per_sm = nb;
+  }
+  const int64_t want = (g.ntiles + NG - 1) / NG;
+  const int64_t cap = static_cast<int64_t>(num_sms_cached()) * blocks_per_sm;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(want < cap ? want : cap));
+  cfg.blockDim = dim3(NG * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, in_map, y_map, xr_map, g, prm);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_error("roundtrip_kernel launch: %s", cudaGetErrorString(e));
+    return ST_ERR_CUDA;
+  }
+  return ST_OK;
+}
+
+// op codes (butterfly.cuh): stage1 | stage2 << 4 | k << 8
+constexpr int kSubF = op_code(ST_DCT2, ST_SUB, 8);      // sub-block post, forward
+constexpr int kSubI = op_code(ST_SUB, ST_IDCT2, 8);     // sub-block post, inverse
+constexpr int kG7F = op_code(ST_GIVENS, ST_DST3, 6);    // band-6 pre DST-7, forward
+constexpr int kG7I = op_code(ST_IDST3, ST_GIVENS, 6);   // band-6 pre DST-7, inverse
+constexpr int kG8F = op_code(ST_GIVENS, ST_IDCT2, 6);   // band-6 pre DCT-8 (DCT-3 base)
+constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS, 6);
+
+#define RT(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, VAR)                \
+  {DT, H, W, RF, CF, RI, CI, VAR,                                                                \
+   &launch_roundtrip<T, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG>}
+
+// variant 0 = default; DCTADJ_RT_VARIANT=k selects tuning variant k where built
+static const RtEntry kRt[] = {
+    // 32x32 fp32, sub-block post (config 2): 8 KB super-tiles, 4 warps x (2 + 1) stages,
+    // 128-register cap (2 CTAs/SM by shared memory); measured variants in profiles/r01_tuning.md
+    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 4, false, 0),
+    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 2, false, 1),
+    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 3, 3, true, true, false, 2, false, 2),
+    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 3, 2, true, true, false, 3, false, 3),
+    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 4),
+    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 4, false, 5),
+    RT(float, DT_F32, 32, 32, 4, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 6),
+    // y stored from registers (no staging tile; measured slower: 0.83 vs 0.90)
+    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 3, true, 7),
+    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 6, true, 8),
+    // 32x32 fp32, band-6 pre (DST-7 / DCT-8 via the DCT-3 base)
+    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 4, false, 0),
+    RT(float, DT_F32, 32, 32, 2, kG8F, kG8F, kG8I, kG8I, 4, 2, true, true, true, 4, false, 0),
+    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 2, false, 1),
+    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 3, 2, true, true, true, 3, false, 2),
+};
+
+#undef RT
+
+const RtEntry* find_roundtrip(int dtype, int h, int w, int rcf, int ccf, int rci, int cci,
+                              int variant) {
+  const RtEntry* dflt = nullptr;
+  for (const RtEntry& e : kRt)
+    if (e.dtype == dtype && e.h == h && e.w == w && e.rcf == rcf && e.ccf == ccf &&
+        e.rci == rci && e.cci == cci) {
+      if (e.variant == variant) return &e;
+      if (e.variant == 0) dflt = &e;
+    }
+  return dflt;
+}
+
+}  // namespace dctadj

@@ -15,7 +15,7 @@ round trip) behind the C-ABI.  New entries:
                                               pipeline.py:236-239), one kernel
   forward_frames / inverse_frames             whole frames tiled into blocks
   forward_adjusted_2d_host / ..._host         host buffers, pipelined copies
-  roundtrip_adjusted_2d_host                  forward + inverse on host buffers, one pass
+  roundtrip_adjusted_2d(_host)                forward + inverse in one kernel (device / host buffers)
   MixedBatch / mixed_forward / mixed_inverse  packed mixed-shape batches (config 3)
 Extension: base DCT-3 is accepted (the DCT-8 pre-adjustment, SURVEY.md App. A
 D3, built with design.flip_pre_adjustment); the reference raises
@@ -237,6 +237,20 @@ def forward_adjusted_2d(th: AdjustedTransform, tv: AdjustedTransform, x):
 def inverse_adjusted_2d(th: AdjustedTransform, tv: AdjustedTransform, y):
     """X = T_v^T Y T_h: columns, then rows (the mirror of the forward)."""
     return _run_2d("dctadj_inverse_2d", th, tv, y)
+
+
+def roundtrip_adjusted_2d(th: AdjustedTransform, tv: AdjustedTransform, x):
+    """(forward_adjusted_2d(x), inverse_adjusted_2d(of that)) in one kernel: x is
+    read once, the coefficients and the reconstruction are written once.  Bit-
+    identical to the two calls.  Returns (y, xr)."""
+    blk, single, as_np = _as_blocks(x, tv.size, th.size)
+    y = _device.empty_like(blk)
+    xr = _device.empty_like(blk)
+    (axh, _kh), (axv, _kv) = th.axis(), tv.axis()
+    _lib.call("dctadj_roundtrip_2d", ctypes.byref(axh), ctypes.byref(axv), blk.data_ptr(),
+              y.data_ptr(), xr.data_ptr(), blk.shape[0], _device.dtype_code(blk),
+              _device.stream_handle())
+    return _debatch(y, single, as_np), _debatch(xr, single, as_np)
 
 
 def _host_out(arr: np.ndarray, out):

@@ -23,7 +23,8 @@ v = torch.randn(3001, 32, device="cuda", generator=g)
 td = benchmark._dense_transform(build_transform(TransformKind.DST7, 32).entries)
 torch.save({"y2": pipeline.forward_adjusted_2d(t, t, x).cpu(),
             "y1": pipeline.forward_adjusted(t, v).cpu(),
-            "yd": pipeline.forward_adjusted_2d(td, td, x).cpu()}, sys.argv[1])
+            "yd": pipeline.forward_adjusted_2d(td, td, x).cpu(),
+            "rt": torch.stack(pipeline.roundtrip_adjusted_2d(t, t, x)).cpu()}, sys.argv[1])
 """
 
 

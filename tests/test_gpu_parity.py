@@ -237,6 +237,68 @@ def test_c2_roundtrip_fp32_integer(golden):
     assert torch.equal(torch.round(xr), x)  # bit-exact integer recovery (D7 iii)
 
 
+# ---------------------------------------------------------------- fused round trip
+def _rt_transforms():
+    s7 = matio.load_designed("sub8_post_dct2_dst7_n32")
+    b6 = matio.load_designed("band6_pre_dst3_dst7_n32")
+    return {"dct8_post": dct8_adjustment_from_dst7(s7), "dst7_post": s7, "dst7_pre": b6,
+            "dct8_pre": flip_pre_adjustment(b6)}
+
+
+@pytest.mark.parametrize("tag", ["dct8_post", "dst7_post", "dst7_pre", "dct8_pre"])
+@pytest.mark.parametrize("nblk", [1, 3, 1000, 4099])
+def test_roundtrip_fused_equals_two_calls(tag, nblk):
+    """One-kernel round trip == forward_adjusted_2d then inverse_adjusted_2d, bit
+    for bit (partial super-tiles included), and y matches the oracle."""
+    adj = _rt_transforms()[tag]
+    t = pipeline.make_adjusted_transform(adj)
+    g = torch.Generator(device="cuda").manual_seed(nblk)
+    x = torch.randn(nblk, 32, 32, device="cuda", generator=g) * 24
+    y, xr = pipeline.roundtrip_adjusted_2d(t, t, x)
+    y2 = pipeline.forward_adjusted_2d(t, t, x)
+    xr2 = pipeline.inverse_adjusted_2d(t, t, y2)
+    assert torch.equal(y, y2) and torch.equal(xr, xr2)
+    assert rel_err(xr.cpu().numpy(), x.cpu().numpy()) < F32_TOL
+    ax = oaxis(adj)
+    k = min(nblk, 64)
+    ref = O.adjusted_2d(ax, ax, x[:k].cpu().numpy().astype(np.float64))
+    assert rel_err(y[:k].cpu().numpy(), ref) < F32_TOL
+
+
+def test_roundtrip_c2_integer_exact_and_fp64(golden):
+    t = pipeline.make_adjusted_transform(_rt_transforms()["dct8_post"])
+    x = dev(golden["c2/x"])
+    y, xr = pipeline.roundtrip_adjusted_2d(t, t, x)
+    assert rel_err(y.cpu().numpy(), golden["c2/y"]) < F32_TOL
+    assert torch.equal(torch.round(xr), x)  # D7 (iii)
+    # fp64 (no fused instantiation: the two-kernel path, same contract)
+    x64 = x.double()
+    y64, xr64 = pipeline.roundtrip_adjusted_2d(t, t, x64)
+    assert rel_err(y64.cpu().numpy(), golden["c2/y"]) < F32_TOL
+    assert torch.equal(y64, pipeline.forward_adjusted_2d(t, t, x64))
+    assert rel_err(xr64.cpu().numpy(), x64.cpu().numpy()) < F64_TOL
+
+
+def test_roundtrip_in_place_and_alias_rule():
+    """xr may alias x (C-ABI); y aliasing xr is rejected before any work."""
+    import ctypes
+    from paper_2505_23618_b200 import _lib
+    t = pipeline.make_adjusted_transform(_rt_transforms()["dct8_post"])
+    x = torch.randn(257, 32, 32, device="cuda") * 24
+    y_ref, xr_ref = pipeline.roundtrip_adjusted_2d(t, t, x)
+    buf = x.clone()
+    y = torch.empty_like(x)
+    (ax, _k) = t.axis()
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.dctadj_roundtrip_2d(ctypes.byref(ax), ctypes.byref(ax), buf.data_ptr(),
+                                       y.data_ptr(), buf.data_ptr(), 257, _lib.F32, st))
+    assert torch.equal(y, y_ref) and torch.equal(buf, xr_ref)
+    with pytest.raises(ValueError):
+        _lib.check(lib.dctadj_roundtrip_2d(ctypes.byref(ax), ctypes.byref(ax), x.data_ptr(),
+                                           y.data_ptr(), y.data_ptr(), 257, _lib.F32, st))
+
+
 def test_c2_host_entry(golden):
     t = pipeline.make_adjusted_transform(
         dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32")))
