@@ -228,7 +228,7 @@ class Uniform(Workload):
 
         self.unfused = [("forward_2d", fwd)] + ([("inverse_2d", inv)] if inverse else [])
         self.launches = self.unfused
-        if fused_roundtrip and inverse:
+        if fused_roundtrip and inverse and lib.dctadj_roundtrip_fused(ref, ref, dtc):
             self.launches = [("roundtrip_2d", rt)]
             self.bytes_first_launch = 3 * coef * es
             self.kernel_name = "roundtrip_kernel"
@@ -564,7 +564,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.config in UNIFORM:
-        w = Uniform(args.config, rank, fused_roundtrip=args.config == "c2" and not args.unfused)
+        w = Uniform(args.config, rank, fused_roundtrip=not args.unfused)
     elif args.config.startswith("c3"):
         w = Mixed(args.config.split("_")[1], rank)
     else:
@@ -748,7 +748,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--unfused", action="store_true",
-                    help="c2: time forward and inverse as two kernels (x, y each cross HBM twice)")
+                    help="fwd+inv configs: time forward and inverse as two kernels (x, y each "
+                         "cross HBM twice) instead of the fused round trip")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=120.0,
                     help="--impl reference: total CPU time budget over warmup + steps")

@@ -117,6 +117,9 @@ int dctadj_inverse_2d(const dctadj_axis* h, const dctadj_axis* v, const void* y,
  * reference's forward_adjusted / inverse_adjusted (pipeline.py:176-191). */
 int dctadj_roundtrip_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
                         void* xr, int64_t nblk, int32_t dtype, void* stream);
+/* 1 when dctadj_roundtrip_2d runs these axes / dtype as the fused kernel, 0
+ * when it runs the two separate kernels (or the arguments are invalid). */
+int dctadj_roundtrip_fused(const dctadj_axis* h, const dctadj_axis* v, int32_t dtype);
 
 /* Host-buffer variants: x_host/y_host are host arrays (pinned for full speed);
  * copies, kernels and read-back are pipelined over chunks on internal streams.

@@ -68,6 +68,7 @@ SIGNATURES = {
     "dctadj_forward_2d": [_AP, _AP, _P, _P, _I64, _I32, _P],
     "dctadj_inverse_2d": [_AP, _AP, _P, _P, _I64, _I32, _P],
     "dctadj_roundtrip_2d": [_AP, _AP, _P, _P, _P, _I64, _I32, _P],
+    "dctadj_roundtrip_fused": [_AP, _AP, _I32],
     "dctadj_forward_2d_host": [_AP, _AP, _P, _P, _I64, _I32, _I32],
     "dctadj_inverse_2d_host": [_AP, _AP, _P, _P, _I64, _I32, _I32],
     "dctadj_roundtrip_2d_host": [_AP, _AP, _P, _P, _P, _I64, _I32, _I32],

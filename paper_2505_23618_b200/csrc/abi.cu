@@ -1441,6 +1441,14 @@ int dctadj_inverse_2d(const dctadj_axis* h, const dctadj_axis* v, const void* y,
                       int64_t nblk, int32_t dtype, void* stream) {
   return run_2d(h, v, y, x, nblk, dtype, true, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, S(stream));
 }
+int dctadj_roundtrip_fused(const dctadj_axis* h, const dctadj_axis* v, int32_t dtype) {
+  AxisPlan fh, fv, ih, iv;
+  if (check_dtype(dtype) || plan_axis(h, false, false, &fh) || plan_axis(v, false, false, &fv) ||
+      plan_axis(h, true, false, &ih) || plan_axis(v, true, false, &iv))
+    return 0;
+  return !rt_unfused() &&
+         find_roundtrip(dtype, fv.n, fh.n, fh.code, fv.code, ih.code, iv.code, rt_variant()) != nullptr;
+}
 int dctadj_roundtrip_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
                         void* xr, int64_t nblk, int32_t dtype, void* stream) {
   return run_roundtrip(h, v, x, y, xr, nblk, dtype, S(stream));

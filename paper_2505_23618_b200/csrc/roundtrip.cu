@@ -7,7 +7,7 @@
 namespace dctadj {
 
 template <typename T, int H, int W, int P, int RCF, int CCF, int RCI, int CCI, int NG, int S,
-          bool PRF, bool PC, bool PRI, int MINB, bool YSTG>
+          bool PRF, bool PC, bool PRI, int MINB, bool YSTG, int NW>
 int launch_roundtrip(const RtArgs& a) {
   using L = TileLayout<T, H, W, P>;
   using Prm = RtParams<T, W, H, RCF, CCF, RCI, CCI>;
@@ -35,7 +35,7 @@ int launch_roundtrip(const RtArgs& a) {
   prm.y = static_cast<T*>(a.y);
   prm.nblk = a.rows / H;
 
-  auto kern = roundtrip_kernel<T, H, W, P, RCF, CCF, RCI, CCI, NG, S, PRF, PC, PRI, MINB, YSTG>;
+  auto kern = roundtrip_kernel<T, H, W, P, RCF, CCF, RCI, CCI, NG, S, PRF, PC, PRI, MINB, YSTG, NW>;
   const size_t smem = 1024 + static_cast<size_t>(NG) * (YSTG ? S : S + 1) * L::STAGEB + NG * S * 8;
   static int blocks_per_sm = 0;  // per instantiation
   if (!blocks_per_sm) {
@@ -45,7 +45,8 @@ int launch_roundtrip(const RtArgs& a) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     int nb = 0;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NG * 32, smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NG * NW * 32, smem);
     if (e != cudaSuccess || nb < 1) {
       set_last_error("roundtrip_kernel setup: %s (%d blocks/SM)", cudaGetErrorString(e), nb);
       return ST_ERR_CUDA;
@@ -56,7 +57,7 @@ int launch_roundtrip(const RtArgs& a) {
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * blocks_per_sm;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(want < cap ? want : cap));
-  cfg.blockDim = dim3(NG * 32);
+  cfg.blockDim = dim3(NG * NW * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = a.stream;
   cudaLaunchAttribute attr[1];
@@ -81,9 +82,11 @@ constexpr int kG7I = op_code(ST_IDST3, ST_GIVENS, 6);   // band-6 pre DST-7, inv
 constexpr int kG8F = op_code(ST_GIVENS, ST_IDCT2, 6);   // band-6 pre DCT-8 (DCT-3 base)
 constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS, 6);
 
-#define RT(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, VAR)                \
+#define RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, NW, VAR)          \
   {DT, H, W, RF, CF, RI, CI, VAR,                                                                \
-   &launch_roundtrip<T, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG>}
+   &launch_roundtrip<T, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, NW>}
+#define RT(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, VAR) \
+  RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, 1, VAR)
 
 // variant 0 = default; DCTADJ_RT_VARIANT=k selects tuning variant k where built
 static const RtEntry kRt[] = {
@@ -104,9 +107,18 @@ static const RtEntry kRt[] = {
     RT(float, DT_F32, 32, 32, 2, kG8F, kG8F, kG8I, kG8I, 4, 2, true, true, true, 4, false, 0),
     RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 2, false, 1),
     RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 3, 2, true, true, true, 3, false, 2),
+    // 64x64 fp32 (config 4): built as tuning variants only -- measured slower than
+    // the two tile kernels (shared memory holds 4-8 warps/SM at 16 KB per block
+    // and 3 buffers per group: sub-8 post 0.52-0.62, band-6 pre 0.44 of the copy
+    // peak vs 0.95 / 0.72 for the two kernels), so the default is the two-kernel path
+    RT(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 1, false, 1),
+    RTW(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, false, false, false, 1, false, 2, 2),
+    RTW(float, DT_F32, 64, 64, 1, kG7F, kG7F, kG7I, kG7I, 4, 2, false, false, false, 1, false, 2, 1),
+    RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 4, 2, false, false, false, 1, false, 2, 1),
 };
 
 #undef RT
+#undef RTW
 
 const RtEntry* find_roundtrip(int dtype, int h, int w, int rcf, int ccf, int rci, int cci,
                               int variant) {

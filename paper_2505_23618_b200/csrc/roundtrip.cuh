@@ -36,12 +36,13 @@ struct RtParams {
 // YSTG: y goes straight from registers to HBM (`yg` = the super-tile's first
 // block, `nb` blocks of it exist): lane c of the warp stores element (i, c), so
 // each store instruction writes whole 128-byte block rows -- no staging tile.
-template <typename T, int H, int W, int P, int CCF, int CCI, int GSQF, bool PAIR, bool YSTG>
+template <typename T, int H, int W, int P, int CCF, int CCI, int GSQF, bool PAIR, bool YSTG,
+          int GT = 32>
 DA_DEV void col_pass_rt(uint8_t* xb, uint8_t* yb, T* yg, int nb, int lane,
                         const typename AxisOp<T, H, CCF>::Coef& cff,
                         const typename AxisOp<T, H, CCI>::Coef& cfi) {
   using L = TileLayout<T, H, W, P>;
-  constexpr int COLS_PER_IT = PAIR ? 64 : 32;
+  constexpr int COLS_PER_IT = PAIR ? 2 * GT : GT;
   static_assert((P * W) % COLS_PER_IT == 0, "column pass must cover whole warps");
 #pragma unroll 1
   for (int it = 0; it < (P * W) / COLS_PER_IT; ++it) {
@@ -93,12 +94,14 @@ DA_DEV void col_pass_rt(uint8_t* xb, uint8_t* yb, T* yg, int nb, int lane,
   }
 }
 
-// NG one-warp groups per CTA; each owns an S-stage ring of input super-tiles and
-// one y staging tile.  Persistent grid, static stride over super-tiles (blocks
-// are independent), programmatic dependent launch like the tile kernel.
+// NG groups of NW warps per CTA; each group owns an S-stage ring of input
+// super-tiles and one y staging tile (NW > 1: a tile's rows / columns are split
+// across the group's warps, which meet at a named barrier).  Persistent grid,
+// static stride over super-tiles (blocks are independent), programmatic
+// dependent launch like the tile kernel.
 template <typename T, int H, int W, int P, int RCF, int CCF, int RCI, int CCI, int NG, int S,
-          bool PAIR_ROW_F, bool PAIR_COL, bool PAIR_ROW_I, int MINB, bool YSTG>
-__global__ void __launch_bounds__(NG * 32, MINB)
+          bool PAIR_ROW_F, bool PAIR_COL, bool PAIR_ROW_I, int MINB, bool YSTG, int NW = 1>
+__global__ void __launch_bounds__(NG * NW * 32, MINB)
     roundtrip_kernel(const __grid_constant__ CUtensorMap in_map,
                      const __grid_constant__ CUtensorMap y_map,
                      const __grid_constant__ CUtensorMap xr_map, const __grid_constant__ Geom geom,
@@ -119,7 +122,9 @@ __global__ void __launch_bounds__(NG * 32, MINB)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
-  const int grp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int GT = NW * 32;
+  static_assert(NW == 1 || NG <= 15, "named barriers 1..15");
+  const int grp = threadIdx.x / GT, lane = threadIdx.x % GT;
   constexpr int NBUF = YSTG ? S : S + 1;  // ring stages (+ the y staging tile)
   uint8_t* ring = smem + grp * NBUF * L::STAGEB;
   uint8_t* ybuf = ring + S * L::STAGEB;
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(NG * 32, MINB)
       prefetch_map(&xr_map);
     }
   }
-  __syncwarp();
+  group_sync<NW>(grp);
 
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * NG + grp;
   const int64_t gstride = static_cast<int64_t>(gridDim.x) * NG;
@@ -157,28 +162,29 @@ __global__ void __launch_bounds__(NG * 32, MINB)
   for (int64_t t = gid, k = 0; t < ntiles; t += gstride, ++k) {
     uint8_t* buf = ring + s * L::STAGEB;
     mbar_wait(&bars[s], phase);
-    row_pass<T, H, W, P, RCF, 1, PAIR_ROW_F>(buf, lane, prm.f.row, nullptr);
+    row_pass<T, H, W, P, RCF, 1, PAIR_ROW_F, GT>(buf, lane, prm.f.row, nullptr);
     if constexpr (!YSTG) {
       // y of the previous tile must have left the staging tile (groups pending
       // at this point: y(k-1), x'(k-1))
       if (lane == 0) bulk_wait_read<1>();
     }
-    __syncwarp();
+    group_sync<NW>(grp);
     const int64_t left = prm.nblk - t * P;
-    col_pass_rt<T, H, W, P, CCF, CCI, GSQF, PAIR_COL, YSTG>(
+    col_pass_rt<T, H, W, P, CCF, CCI, GSQF, PAIR_COL, YSTG, GT>(
         buf, ybuf, prm.y + static_cast<size_t>(t) * P * H * W, left < P ? static_cast<int>(left) : P,
         lane, prm.f.col, prm.i.col);
     if constexpr (!YSTG) {
       fence_proxy_async_smem();
-      __syncwarp();
+      group_sync<NW>(grp);
       if (lane == 0) {
         issue_tile_io<T, H, W, P, MODE_LINEAR>(false, ybuf, &y_map, nullptr, t, geom, P);
         bulk_commit();
       }
     }
-    row_pass<T, H, W, P, RCI, GSQI, PAIR_ROW_I>(buf, lane, prm.i.row, nullptr);
+    if constexpr (YSTG) group_sync<NW>(grp);  // the column pass is complete
+    row_pass<T, H, W, P, RCI, GSQI, PAIR_ROW_I, GT>(buf, lane, prm.i.row, nullptr);
     fence_proxy_async_smem();
-    __syncwarp();
+    group_sync<NW>(grp);
     if (lane == 0) {
       issue_tile_io<T, H, W, P, MODE_LINEAR>(false, buf, &xr_map, nullptr, t, geom, P);
       bulk_commit();
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(NG * 32, MINB)
         }
       }
     }
-    __syncwarp();
+    group_sync<NW>(grp);
     if (++s == S) {
       s = 0;
       phase ^= 1;

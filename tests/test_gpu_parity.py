@@ -238,22 +238,22 @@ def test_c2_roundtrip_fp32_integer(golden):
 
 
 # ---------------------------------------------------------------- fused round trip
-def _rt_transforms():
-    s7 = matio.load_designed("sub8_post_dct2_dst7_n32")
-    b6 = matio.load_designed("band6_pre_dst3_dst7_n32")
+def _rt_transforms(n=32):
+    s7 = matio.load_designed(f"sub8_post_dct2_dst7_n{n}")
+    b6 = matio.load_designed(f"band6_pre_dst3_dst7_n{n}")
     return {"dct8_post": dct8_adjustment_from_dst7(s7), "dst7_post": s7, "dst7_pre": b6,
             "dct8_pre": flip_pre_adjustment(b6)}
 
 
 @pytest.mark.parametrize("tag", ["dct8_post", "dst7_post", "dst7_pre", "dct8_pre"])
-@pytest.mark.parametrize("nblk", [1, 3, 1000, 4099])
-def test_roundtrip_fused_equals_two_calls(tag, nblk):
+@pytest.mark.parametrize("n,nblk", [(32, 1), (32, 3), (32, 1000), (32, 4099), (64, 1), (64, 777)])
+def test_roundtrip_fused_equals_two_calls(tag, n, nblk):
     """One-kernel round trip == forward_adjusted_2d then inverse_adjusted_2d, bit
     for bit (partial super-tiles included), and y matches the oracle."""
-    adj = _rt_transforms()[tag]
+    adj = _rt_transforms(n)[tag]
     t = pipeline.make_adjusted_transform(adj)
     g = torch.Generator(device="cuda").manual_seed(nblk)
-    x = torch.randn(nblk, 32, 32, device="cuda", generator=g) * 24
+    x = torch.randn(nblk, n, n, device="cuda", generator=g) * 24
     y, xr = pipeline.roundtrip_adjusted_2d(t, t, x)
     y2 = pipeline.forward_adjusted_2d(t, t, x)
     xr2 = pipeline.inverse_adjusted_2d(t, t, y2)

@@ -267,3 +267,25 @@ def test_library_resolves_all_symbols_eagerly():
     if not _lib.LIB_PATH.exists():
         pytest.skip("libdctadj.so not built")
     ctypes.CDLL(str(_lib.LIB_PATH), mode=os.RTLD_NOW)
+
+
+def test_roundtrip_fused_query():
+    """dctadj_roundtrip_fused says which round trips run as the one fused kernel
+    (host-side planning only, no device work)."""
+    if not _lib.LIB_PATH.exists():
+        pytest.skip("libdctadj.so not built")
+    from paper_2505_23618_b200 import pipeline
+    from paper_2505_23618_b200.design import dct8_adjustment_from_dst7
+    lib = _lib.load()
+
+    def fused(name, dtype, c8=False):
+        adj = matio.load_designed(name)
+        t = pipeline.make_adjusted_transform(dct8_adjustment_from_dst7(adj) if c8 else adj)
+        ax, _keep = t.axis()
+        return lib.dctadj_roundtrip_fused(ctypes.byref(ax), ctypes.byref(ax), dtype)
+
+    assert fused("sub8_post_dct2_dst7_n32", _lib.F32, c8=True) == 1   # config 2
+    assert fused("band6_pre_dst3_dst7_n32", _lib.F32) == 1
+    assert fused("sub8_post_dct2_dst7_n32", _lib.F64) == 0           # fp64: two kernels
+    assert fused("sub8_post_dct2_dst7_n64", _lib.F32) == 0           # 64x64: two kernels
+    assert fused("sub8_post_dct2_dst7_n32", 7) == 0                  # invalid dtype
