@@ -7,7 +7,7 @@
 namespace dctadj {
 
 template <typename T, int H, int W, int P, int RCF, int CCF, int RCI, int CCI, int NG, int S,
-          bool PRF, bool PC, bool PRI, int MINB, bool YSTG, int NW>
+          bool PRF, bool PC, bool PRI, int MINB, bool YSTG, int NW, int CH = 0>
 int launch_roundtrip(const RtArgs& a) {
   using L = TileLayout<T, H, W, P>;
   using Prm = RtParams<T, W, H, RCF, CCF, RCI, CCI>;
@@ -35,7 +35,7 @@ int launch_roundtrip(const RtArgs& a) {
   prm.y = static_cast<T*>(a.y);
   prm.nblk = a.rows / H;
 
-  auto kern = roundtrip_kernel<T, H, W, P, RCF, CCF, RCI, CCI, NG, S, PRF, PC, PRI, MINB, YSTG, NW>;
+  auto kern = roundtrip_kernel<T, H, W, P, RCF, CCF, RCI, CCI, NG, S, PRF, PC, PRI, MINB, YSTG, NW, CH>;
   const size_t smem = 1024 + static_cast<size_t>(NG) * (YSTG ? S : S + 1) * L::STAGEB + NG * S * 8;
   static int blocks_per_sm = 0;  // per instantiation
   if (!blocks_per_sm) {
@@ -99,6 +99,7 @@ static const RtEntry kRt[] = {
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 4),
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 4, false, 5),
     RT(float, DT_F32, 32, 32, 4, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 6),
+    // (L2 evict-first hints on the loads, the stores or both: no change, 137.9-139.1 us)
     // y stored from registers (no staging tile; measured slower: 0.83 vs 0.90)
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 3, true, 7),
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 6, true, 8),

@@ -100,7 +100,8 @@ DA_DEV void col_pass_rt(uint8_t* xb, uint8_t* yb, T* yg, int nb, int lane,
 // static stride over super-tiles (blocks are independent), programmatic
 // dependent launch like the tile kernel.
 template <typename T, int H, int W, int P, int RCF, int CCF, int RCI, int CCI, int NG, int S,
-          bool PAIR_ROW_F, bool PAIR_COL, bool PAIR_ROW_I, int MINB, bool YSTG, int NW = 1>
+          bool PAIR_ROW_F, bool PAIR_COL, bool PAIR_ROW_I, int MINB, bool YSTG, int NW = 1,
+          int CH = 0>  // CH: L2 hints, 1 = loads evict_first, 2 = stores evict_first
 __global__ void __launch_bounds__(NG * NW * 32, MINB)
     roundtrip_kernel(const __grid_constant__ CUtensorMap in_map,
                      const __grid_constant__ CUtensorMap y_map,
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
       const int64_t t = gid + s * gstride;
       if (t < ntiles) {
         mbar_arrive_expect_tx(&bars[s], L::TILEB);
-        issue_tile_io<T, H, W, P, MODE_LINEAR>(true, ring + s * L::STAGEB, &in_map, &bars[s], t,
+        issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(true, ring + s * L::STAGEB, &in_map, &bars[s], t,
                                                geom, P);
       }
     }
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
       fence_proxy_async_smem();
       group_sync<NW>(grp);
       if (lane == 0) {
-        issue_tile_io<T, H, W, P, MODE_LINEAR>(false, ybuf, &y_map, nullptr, t, geom, P);
+        issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(false, ybuf, &y_map, nullptr, t, geom, P);
         bulk_commit();
       }
     }
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
     fence_proxy_async_smem();
     group_sync<NW>(grp);
     if (lane == 0) {
-      issue_tile_io<T, H, W, P, MODE_LINEAR>(false, buf, &xr_map, nullptr, t, geom, P);
+      issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(false, buf, &xr_map, nullptr, t, geom, P);
       bulk_commit();
       // refill the stage of the previous tile with the tile S-1 strides ahead,
       // once its x' store has read it (pending after that: [y(k),] x'(k))
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
           const int sp = (s == 0) ? S - 1 : s - 1;
           bulk_wait_read<YSTG ? 1 : 2>();
           mbar_arrive_expect_tx(&bars[sp], L::TILEB);
-          issue_tile_io<T, H, W, P, MODE_LINEAR>(true, ring + sp * L::STAGEB, &in_map, &bars[sp],
+          issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(true, ring + sp * L::STAGEB, &in_map, &bars[sp],
                                                  tn, geom, P);
         }
       }

@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-for c in c4_dst7_post c1; do timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['value']/1e9,1), round(d['roofline']['frac'],3), d['roofline']['per_launch_ms'])"; done > gpurun_out/bench_c4c1.log 2>&1
+for v in 0 9 10 11 0; do echo "v$v"; DCTADJ_RT_VARIANT=$v timeout 300 python tools/prof_rt.py 100; done > gpurun_out/prof_rt_hints.log 2>&1
