@@ -297,7 +297,7 @@ class Uniform(Workload):
 class Mixed(Workload):
     """Config 3: 1,048,576 blocks, shapes {16,32}^2 and (h, v) kinds uniform."""
 
-    def __init__(self, side: str, rank: int, nblk: int = 1 << 20):
+    def __init__(self, side: str, rank: int, nblk: int = 1 << 20, fused_roundtrip: bool = False):
         import torch
         from paper_2505_23618_b200 import _lib, pipeline, workloads
         self.workload = f"c3_mixed_{side}_fwd+inv_{nblk}blocks"
@@ -345,8 +345,19 @@ class Mixed(Workload):
         def inv():
             _lib.check(lib.dctadj_mixed_inverse(plan, self.axes, self.y.data_ptr(), self.xr.data_ptr(), 0, st))
 
-        self.launches = [("mixed_forward", fwd), ("mixed_inverse", inv)]
-        self.kernels_per_step = 2 * len(self.batch_classes(h_index, v_index))
+        def rt():  # one fused gather kernel per class: x read once, y and x' written once
+            _lib.check(lib.dctadj_mixed_roundtrip(plan, self.axes, self.x.data_ptr(), self.y.data_ptr(),
+                                                  self.xr.data_ptr(), 0, st))
+
+        self.unfused = [("mixed_forward", fwd), ("mixed_inverse", inv)]
+        self.launches = self.unfused
+        nclass = len(self.batch_classes(h_index, v_index))
+        self.kernels_per_step = 2 * nclass
+        if fused_roundtrip and lib.dctadj_mixed_roundtrip_fused(plan, self.axes, 0):
+            self.launches = [("mixed_roundtrip", rt)]
+            self.kernels_per_step = nclass
+            self.bytes_first_launch = 3 * total * 4
+            self.kernel_name = "roundtrip_kernel (gather, one per class)"
         self.h_index, self.v_index = h_index, v_index
         self.extra = {"blocks_per_gpu": nblk, "coefficients_per_gpu": total,
                       "classes": int(len(np.unique(h_index * 4 + v_index))),
@@ -566,7 +577,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if args.config in UNIFORM:
         w = Uniform(args.config, rank, fused_roundtrip=not args.unfused)
     elif args.config.startswith("c3"):
-        w = Mixed(args.config.split("_")[1], rank)
+        w = Mixed(args.config.split("_")[1], rank, fused_roundtrip=not args.unfused)
     else:
         w = Frames(rank, world)
     torch.cuda.synchronize()

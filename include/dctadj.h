@@ -188,6 +188,15 @@ int dctadj_mixed_forward(const dctadj_mixed* plan, const dctadj_axis* table, con
                          void* y, int32_t dtype, void* stream);
 int dctadj_mixed_inverse(const dctadj_mixed* plan, const dctadj_axis* table, const void* y,
                          void* x, int32_t dtype, void* stream);
+/* forward then inverse of the whole mixed batch (y = forward(x), xr =
+ * inverse(y)) with one fused gather kernel per class (x read once, y and xr
+ * written once); bit-identical to dctadj_mixed_forward + dctadj_mixed_inverse,
+ * which it runs when a class has no fused kernel.  y must not alias xr. */
+int dctadj_mixed_roundtrip(const dctadj_mixed* plan, const dctadj_axis* table, const void* x,
+                           void* y, void* xr, int32_t dtype, void* stream);
+/* 1 when dctadj_mixed_roundtrip runs this plan / table / dtype as fused kernels */
+int dctadj_mixed_roundtrip_fused(const dctadj_mixed* plan, const dctadj_axis* table,
+                                 int32_t dtype);
 int dctadj_mixed_destroy(dctadj_mixed* plan);
 
 /* ---- diagnostics ---- */

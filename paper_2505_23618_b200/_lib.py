@@ -80,6 +80,8 @@ SIGNATURES = {
     "dctadj_mixed_create": [_P, _P, _P, _I64, _P, _I32, _I64, ctypes.POINTER(_P)],
     "dctadj_mixed_forward": [_P, _AP, _P, _P, _I32, _P],
     "dctadj_mixed_inverse": [_P, _AP, _P, _P, _I32, _P],
+    "dctadj_mixed_roundtrip": [_P, _AP, _P, _P, _P, _I32, _P],
+    "dctadj_mixed_roundtrip_fused": [_P, _AP, _I32],
     "dctadj_mixed_destroy": [_P],
     "dctadj_status_string": [_I32],
     "dctadj_last_error": [],

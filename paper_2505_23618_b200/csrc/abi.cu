@@ -851,7 +851,7 @@ static int run_roundtrip(const dctadj_axis* h, const dctadj_axis* v, const void*
   const int H = fv.n, W = fh.n;
   const RtEntry* e = rt_unfused() ? nullptr
                                   : find_roundtrip(dtype, H, W, fh.code, fv.code, ih.code, iv.code,
-                                                   rt_variant());
+                                                   MODE_LINEAR, rt_variant());
   if (trace_on())
     std::fprintf(stderr, "[dctadj] roundtrip dtype=%d %dx%d ops 0x%x/0x%x/0x%x/0x%x: %s\n", dtype, H,
                  W, fh.code, fv.code, ih.code, iv.code, e ? "fused" : "two kernels");
@@ -1304,6 +1304,85 @@ static int run_mixed(const dctadj_mixed* plan, const dctadj_axis* table, const v
   return ST_OK;
 }
 
+struct MixedRtClass {
+  const RtEntry* e = nullptr;
+  AxisPlan fh, fv, ih, iv;
+};
+// the fused gather kernel of every class, or *fused = false when one is missing
+static int plan_mixed_roundtrip(const dctadj_mixed* plan, const dctadj_axis* table, int dtype,
+                                std::vector<MixedRtClass>& runs, bool* fused) {
+  runs.assign(plan->classes.size(), MixedRtClass());
+  *fused = !rt_unfused();
+  for (size_t i = 0; i < plan->classes.size() && *fused; ++i) {
+    const auto& c = plan->classes[i];
+    const dctadj_axis* h = &table[c.h_index];
+    const dctadj_axis* v = &table[c.v_index];
+    MixedRtClass& r = runs[i];
+    int rc;
+    if ((rc = plan_axis(h, false, false, &r.fh)) || (rc = plan_axis(v, false, false, &r.fv)) ||
+        (rc = plan_axis(h, true, false, &r.ih)) || (rc = plan_axis(v, true, false, &r.iv)))
+      return rc;
+    r.e = find_roundtrip(dtype, v->n, h->n, r.fh.code, r.fv.code, r.ih.code, r.iv.code,
+                         MODE_GATHER, rt_variant());
+    *fused = r.e != nullptr;
+  }
+  return ST_OK;
+}
+
+// Mixed batch round trip: y = forward(x), xr = inverse(y) per class as ONE
+// fused gather kernel (roundtrip.cuh) when every class has one, else the
+// forward and inverse mixed runs back to back (identical results).
+static int run_mixed_roundtrip(const dctadj_mixed* plan, const dctadj_axis* table, const void* x,
+                               void* y, void* xr, int dtype, cudaStream_t st) {
+  int rc = check_dtype(dtype);
+  if (rc) return rc;
+  if (!plan || !table) return fail(ST_ERR_VALUE, "NULL plan or axis table");
+  for (size_t k = 0; k < plan->sizes.size(); ++k) {
+    if ((rc = validate_axis(&table[k])) != ST_OK) return rc;
+    if (table[k].n != plan->sizes[k])
+      return fail(ST_ERR_SHAPE, "axis table entry %zu has n=%d, plan built for %d", k,
+                  table[k].n, plan->sizes[k]);
+  }
+  if (plan->nblk == 0) return ST_OK;
+  if (!x || !y || !xr) return fail(ST_ERR_VALUE, "NULL data pointer");
+  if (y == xr) return fail(ST_ERR_VALUE, "coefficients and reconstruction must not alias");
+  std::vector<MixedRtClass> runs;
+  bool fused = false;
+  if ((rc = plan_mixed_roundtrip(plan, table, dtype, runs, &fused))) return rc;
+  if (trace_on())
+    std::fprintf(stderr, "[dctadj] mixed roundtrip: %s\n", fused ? "fused" : "two passes");
+  if (!fused) {
+    rc = run_mixed(plan, table, x, y, dtype, false, st);
+    return rc ? rc : run_mixed(plan, table, y, xr, dtype, true, st);
+  }
+  DA_CUDA(cudaEventRecord(plan->fork, st));
+  for (int i = 0; i < dctadj_mixed::NSTREAM; ++i) DA_CUDA(cudaStreamWaitEvent(plan->aux[i], plan->fork, 0));
+  for (size_t i = 0; i < plan->classes.size(); ++i) {
+    const auto& c = plan->classes[i];
+    const MixedRtClass& r = runs[i];
+    const std::vector<unsigned char> c0 = to_dtype(r.fh.coef, dtype), c1 = to_dtype(r.fv.coef, dtype),
+                                     c2 = to_dtype(r.ih.coef, dtype), c3 = to_dtype(r.iv.coef, dtype);
+    RtArgs a;
+    a.in = x;
+    a.y = y;
+    a.xr = xr;
+    a.rows = plan->total_elements / r.fh.n;
+    a.coef[0] = c0.data();
+    a.coef[1] = c1.data();
+    a.coef[2] = c2.data();
+    a.coef[3] = c3.data();
+    a.offsets = c.offsets;
+    a.gather_blocks = c.count;
+    a.stream = plan->aux[i % dctadj_mixed::NSTREAM];
+    if ((rc = r.e->fn(a))) return rc;
+  }
+  for (int i = 0; i < dctadj_mixed::NSTREAM; ++i) {
+    DA_CUDA(cudaEventRecord(plan->join[i], plan->aux[i]));
+    DA_CUDA(cudaStreamWaitEvent(st, plan->join[i], 0));
+  }
+  return ST_OK;
+}
+
 // generic rectangular dense product (rows != n), the one path off the tile kernel
 template <typename T>
 __global__ void dense_rect_kernel(const T* __restrict__ m, int rows, const T* __restrict__ x,
@@ -1447,7 +1526,8 @@ int dctadj_roundtrip_fused(const dctadj_axis* h, const dctadj_axis* v, int32_t d
       plan_axis(h, true, false, &ih) || plan_axis(v, true, false, &iv))
     return 0;
   return !rt_unfused() &&
-         find_roundtrip(dtype, fv.n, fh.n, fh.code, fv.code, ih.code, iv.code, rt_variant()) != nullptr;
+         find_roundtrip(dtype, fv.n, fh.n, fh.code, fv.code, ih.code, iv.code, MODE_LINEAR,
+                        rt_variant()) != nullptr;
 }
 int dctadj_roundtrip_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, void* y,
                         void* xr, int64_t nblk, int32_t dtype, void* stream) {
@@ -1590,6 +1670,19 @@ int dctadj_mixed_forward(const dctadj_mixed* plan, const dctadj_axis* table, con
 int dctadj_mixed_inverse(const dctadj_mixed* plan, const dctadj_axis* table, const void* y,
                          void* x, int32_t dtype, void* stream) {
   return run_mixed(plan, table, y, x, dtype, true, S(stream));
+}
+int dctadj_mixed_roundtrip(const dctadj_mixed* plan, const dctadj_axis* table, const void* x,
+                           void* y, void* xr, int32_t dtype, void* stream) {
+  return run_mixed_roundtrip(plan, table, x, y, xr, dtype, S(stream));
+}
+int dctadj_mixed_roundtrip_fused(const dctadj_mixed* plan, const dctadj_axis* table,
+                                 int32_t dtype) {
+  if (!plan || !table || check_dtype(dtype)) return 0;
+  for (size_t k = 0; k < plan->sizes.size(); ++k)
+    if (validate_axis(&table[k]) != ST_OK || table[k].n != plan->sizes[k]) return 0;
+  std::vector<MixedRtClass> runs;
+  bool fused = false;
+  return plan_mixed_roundtrip(plan, table, dtype, runs, &fused) == ST_OK && fused;
 }
 int dctadj_mixed_destroy(dctadj_mixed* plan) {
   if (!plan) return ST_OK;

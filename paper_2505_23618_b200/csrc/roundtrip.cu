@@ -7,20 +7,27 @@
 namespace dctadj {
 
 template <typename T, int H, int W, int P, int RCF, int CCF, int RCI, int CCI, int NG, int S,
-          bool PRF, bool PC, bool PRI, int MINB, bool YSTG, int NW, int CH = 0>
+          bool PRF, bool PC, bool PRI, int MINB, bool YSTG, int NW, int CH = 0,
+          int MODE = MODE_LINEAR>
 int launch_roundtrip(const RtArgs& a) {
   using L = TileLayout<T, H, W, P>;
   using Prm = RtParams<T, W, H, RCF, CCF, RCI, CCI>;
   Geom g{};
-  g.ntiles = (a.rows + L::PH - 1) / L::PH;
-  g.nblocks = g.ntiles * P;
+  if constexpr (MODE == MODE_GATHER) {
+    g.nblocks = a.gather_blocks;
+    g.ntiles = (g.nblocks + P - 1) / P;
+    g.offsets = a.offsets;
+  } else {
+    g.ntiles = (a.rows + L::PH - 1) / L::PH;
+    g.nblocks = g.ntiles * P;
+  }
   if (g.ntiles == 0) return ST_OK;
   LaunchArgs la;
   la.rows = a.rows;
   CUtensorMap in_map, y_map, xr_map;
-  int rc = make_map<T, H, W, P, MODE_LINEAR>(&in_map, a.in, la);
-  if (!rc) rc = make_map<T, H, W, P, MODE_LINEAR>(&y_map, a.y, la);
-  if (!rc) rc = make_map<T, H, W, P, MODE_LINEAR>(&xr_map, a.xr, la);
+  int rc = make_map<T, H, W, P, MODE>(&in_map, a.in, la);
+  if (!rc) rc = make_map<T, H, W, P, MODE>(&y_map, a.y, la);
+  if (!rc) rc = make_map<T, H, W, P, MODE>(&xr_map, a.xr, la);
   if (rc) return rc;
   Prm prm;
   std::memset(&prm, 0, sizeof(prm));
@@ -35,7 +42,8 @@ int launch_roundtrip(const RtArgs& a) {
   prm.y = static_cast<T*>(a.y);
   prm.nblk = a.rows / H;
 
-  auto kern = roundtrip_kernel<T, H, W, P, RCF, CCF, RCI, CCI, NG, S, PRF, PC, PRI, MINB, YSTG, NW, CH>;
+  auto kern =
+      roundtrip_kernel<T, H, W, P, RCF, CCF, RCI, CCI, NG, S, PRF, PC, PRI, MINB, YSTG, NW, CH, MODE>;
   const size_t smem = 1024 + static_cast<size_t>(NG) * (YSTG ? S : S + 1) * L::STAGEB + NG * S * 8;
   static int blocks_per_sm = 0;  // per instantiation
   if (!blocks_per_sm) {
@@ -83,8 +91,15 @@ constexpr int kG8F = op_code(ST_GIVENS, ST_IDCT2, 6);   // band-6 pre DCT-8 (DCT
 constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS, 6);
 
 #define RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, NW, VAR)          \
-  {DT, H, W, RF, CF, RI, CI, VAR,                                                                \
+  {DT, H, W, RF, CF, RI, CI, MODE_LINEAR, VAR,                                                   \
    &launch_roundtrip<T, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, NW>}
+// mixed-shape gather kernels (config 3): 8 KB super-tiles of one class, 4 warps x (2 + 1)
+#define RTGV(H, W, RF, CF, RI, CI, PRI, NG, MINB, VAR)                                            \
+  {DT_F32, H, W, RF, CF, RI, CI, MODE_GATHER, VAR,                                               \
+   &launch_roundtrip<float, H, W, 2048 / (H * W), RF, CF, RI, CI, NG, 2, true, true, PRI, MINB,    \
+                     false, 1, 0, MODE_GATHER>}
+#define RTG(H, W, RF, CF, RI, CI, PRI, VAR) RTGV(H, W, RF, CF, RI, CI, PRI, 4, 4, VAR), \
+  RTGV(H, W, RF, CF, RI, CI, PRI, 4, 2, VAR + 1), RTGV(H, W, RF, CF, RI, CI, PRI, 3, 3, VAR + 2)
 #define RT(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, VAR) \
   RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, 1, VAR)
 
@@ -116,17 +131,33 @@ static const RtEntry kRt[] = {
     RTW(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, false, false, false, 1, false, 2, 2),
     RTW(float, DT_F32, 64, 64, 1, kG7F, kG7F, kG7I, kG7I, 4, 2, false, false, false, 1, false, 2, 1),
     RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 4, 2, false, false, false, 1, false, 2, 1),
+    // config 3 classes: {16,32}^2 shapes, sub-block post (DST-7 / DCT-8 share the ops) and
+    // band-6 pre with DST-7 or DCT-8 per axis
+    RTG(16, 16, kSubF, kSubF, kSubI, kSubI, false, 0),
+    RTG(16, 32, kSubF, kSubF, kSubI, kSubI, false, 0),
+    RTG(32, 16, kSubF, kSubF, kSubI, kSubI, false, 0),
+    RTG(32, 32, kSubF, kSubF, kSubI, kSubI, false, 0),
+#define RTG_PRE(H, W)                                      \
+  RTG(H, W, kG7F, kG7F, kG7I, kG7I, true, 0), RTG(H, W, kG7F, kG8F, kG7I, kG8I, true, 0), \
+      RTG(H, W, kG8F, kG7F, kG8I, kG7I, true, 0), RTG(H, W, kG8F, kG8F, kG8I, kG8I, true, 0)
+    RTG_PRE(16, 16),
+    RTG_PRE(16, 32),
+    RTG_PRE(32, 16),
+    RTG_PRE(32, 32),
+#undef RTG_PRE
 };
 
 #undef RT
 #undef RTW
+#undef RTG
+#undef RTGV
 
 const RtEntry* find_roundtrip(int dtype, int h, int w, int rcf, int ccf, int rci, int cci,
-                              int variant) {
+                              int mode, int variant) {
   const RtEntry* dflt = nullptr;
   for (const RtEntry& e : kRt)
     if (e.dtype == dtype && e.h == h && e.w == w && e.rcf == rcf && e.ccf == ccf &&
-        e.rci == rci && e.cci == cci) {
+        e.rci == rci && e.cci == cci && e.mode == mode) {
       if (e.variant == variant) return &e;
       if (e.variant == 0) dflt = &e;
     }

@@ -101,7 +101,8 @@ DA_DEV void col_pass_rt(uint8_t* xb, uint8_t* yb, T* yg, int nb, int lane,
 // dependent launch like the tile kernel.
 template <typename T, int H, int W, int P, int RCF, int CCF, int RCI, int CCI, int NG, int S,
           bool PAIR_ROW_F, bool PAIR_COL, bool PAIR_ROW_I, int MINB, bool YSTG, int NW = 1,
-          int CH = 0>  // CH: L2 hints, 1 = loads evict_first, 2 = stores evict_first
+          int CH = 0,  // CH: L2 hints, 1 = loads evict_first, 2 = stores evict_first
+          int MODE = MODE_LINEAR>
 __global__ void __launch_bounds__(NG * NW * 32, MINB)
     roundtrip_kernel(const __grid_constant__ CUtensorMap in_map,
                      const __grid_constant__ CUtensorMap y_map,
@@ -146,17 +147,52 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * NG + grp;
   const int64_t gstride = static_cast<int64_t>(gridDim.x) * NG;
   const int64_t ntiles = geom.ntiles;
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int64_t t = gid + s * gstride;
-      if (t < ntiles) {
-        mbar_arrive_expect_tx(&bars[s], L::TILEB);
-        issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(true, ring + s * L::STAGEB, &in_map, &bars[s], t,
-                                               geom, P);
-      }
+  // GATHER (config 3): one TMA box per block at its element offset in a packed
+  // mixed-shape buffer; lane p < P moves block p of every super-tile (loads and
+  // both stores), so each lane's bulk-group accounting covers its own block.
+  // The offsets of the tiles in flight are kept per stage, the next refill's
+  // prefetched into a register.
+  constexpr bool GATHER = MODE == MODE_GATHER;
+  static_assert(MODE == MODE_LINEAR || MODE == MODE_GATHER, "linear or gather batches");
+  static_assert(!GATHER || (!YSTG && P <= GT), "gather: staged y, one lane per block");
+  __shared__ int64_t goffs[GATHER ? NG * S * P : 1];
+  int64_t* my_offs = goffs + (GATHER ? grp * S * P : 0);
+  int64_t pref = 0;
+  auto load = [&](int st, int64_t t, int64_t off) {  // GATHER: every lane; else lane 0
+    const int nb = tile_blocks<P, MODE>(t, geom);
+    if constexpr (GATHER) {
+      if (lane == 0) mbar_arrive_expect_tx(&bars[st], L::TILEB / P * nb);
+      group_sync<NW>(grp);
+      if (lane < P) my_offs[st * P + lane] = off;
+      gather_io<T, H, W, P>(true, ring + st * L::STAGEB, &in_map, &bars[st], lane, nb, off);
+    } else {
+      mbar_arrive_expect_tx(&bars[st], L::TILEB);
+      issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(true, ring + st * L::STAGEB, &in_map, &bars[st],
+                                                 t, geom, P);
     }
+  };
+  auto store = [&](const CUtensorMap* map, uint8_t* src, int st, int64_t t) {
+    if constexpr (GATHER) {
+      gather_io<T, H, W, P>(false, src, map, nullptr, lane, tile_blocks<P, MODE>(t, geom),
+                            lane < P ? my_offs[st * P + lane] : 0);
+      bulk_commit();
+    } else if (lane == 0) {
+      issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(false, src, map, nullptr, t, geom, P);
+      bulk_commit();
+    }
+  };
+  auto offset_of = [&](int64_t t) -> int64_t {  // GATHER: this lane's block of tile t
+    if constexpr (GATHER)
+      return (t < ntiles && lane < tile_blocks<P, MODE>(t, geom)) ? geom.offsets[t * P + lane] : 0;
+    else
+      return 0;
+  };
+#pragma unroll
+  for (int st = 0; st < S; ++st) {
+    const int64_t t = gid + st * gstride;
+    if (t < ntiles && (GATHER || lane == 0)) load(st, t, offset_of(t));
   }
+  if constexpr (GATHER) pref = offset_of(gid + S * gstride);
 
   int s = 0;
   uint32_t phase = 0;
@@ -167,7 +203,7 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
     if constexpr (!YSTG) {
       // y of the previous tile must have left the staging tile (groups pending
       // at this point: y(k-1), x'(k-1))
-      if (lane == 0) bulk_wait_read<1>();
+      if (GATHER || lane == 0) bulk_wait_read<1>();
     }
     group_sync<NW>(grp);
     const int64_t left = prm.nblk - t * P;
@@ -177,29 +213,22 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
     if constexpr (!YSTG) {
       fence_proxy_async_smem();
       group_sync<NW>(grp);
-      if (lane == 0) {
-        issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(false, ybuf, &y_map, nullptr, t, geom, P);
-        bulk_commit();
-      }
+      store(&y_map, ybuf, s, t);
     }
     if constexpr (YSTG) group_sync<NW>(grp);  // the column pass is complete
     row_pass<T, H, W, P, RCI, GSQI, PAIR_ROW_I, GT>(buf, lane, prm.i.row, nullptr);
     fence_proxy_async_smem();
     group_sync<NW>(grp);
-    if (lane == 0) {
-      issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(false, buf, &xr_map, nullptr, t, geom, P);
-      bulk_commit();
-      // refill the stage of the previous tile with the tile S-1 strides ahead,
-      // once its x' store has read it (pending after that: [y(k),] x'(k))
-      if (k >= 1) {
-        const int64_t tn = t + (S - 1) * gstride;
-        if (tn < ntiles) {
-          const int sp = (s == 0) ? S - 1 : s - 1;
-          bulk_wait_read<YSTG ? 1 : 2>();
-          mbar_arrive_expect_tx(&bars[sp], L::TILEB);
-          issue_tile_io<T, H, W, P, MODE_LINEAR, CH>(true, ring + sp * L::STAGEB, &in_map, &bars[sp],
-                                                 tn, geom, P);
-        }
+    store(&xr_map, buf, s, t);
+    // refill the stage of the previous tile with the tile S-1 strides ahead,
+    // once its x' store has read it (pending after that: [y(k),] x'(k))
+    if (k >= 1) {
+      const int64_t tn = t + (S - 1) * gstride;
+      if (tn < ntiles && (GATHER || lane == 0)) {
+        const int sp = (s == 0) ? S - 1 : s - 1;
+        bulk_wait_read<YSTG ? 1 : 2>();
+        load(sp, tn, pref);
+        if constexpr (GATHER) pref = offset_of(tn + gstride);
       }
     }
     group_sync<NW>(grp);
@@ -208,7 +237,7 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
       phase ^= 1;
     }
   }
-  if (lane == 0) bulk_wait_all();
+  if (GATHER || lane == 0) bulk_wait_all();
 }
 
 }  // namespace dctadj
@@ -220,18 +249,21 @@ struct RtArgs {
   const void* in = nullptr;  // x   (rows x W, LINEAR)
   void* y = nullptr;         // y   (forward coefficients)
   void* xr = nullptr;        // x'  (reconstruction)
-  int64_t rows = 0;          // nblk * H
+  int64_t rows = 0;          // LINEAR: nblk * H; GATHER: rows of W in the packed buffer
   const void* coef[4] = {};  // host, packed Coef of: forward row, forward column, inverse row, inverse column
+  const int64_t* offsets = nullptr;  // GATHER: device, element offset of each block
+  int64_t gather_blocks = 0;         // GATHER: blocks of this class
   cudaStream_t stream = nullptr;
 };
 
 struct RtEntry {
-  int dtype, h, w, rcf, ccf, rci, cci, variant;
+  int dtype, h, w, rcf, ccf, rci, cci, mode, variant;
   int (*fn)(const RtArgs&);
 };
 
-// implemented in roundtrip.cu: the fused kernel for these ops, or nullptr
+// implemented in roundtrip.cu: the fused kernel for these ops and addressing
+// mode (MODE_LINEAR / MODE_GATHER), or nullptr
 const RtEntry* find_roundtrip(int dtype, int h, int w, int rcf, int ccf, int rci, int cci,
-                              int variant);
+                              int mode, int variant);
 
 }  // namespace dctadj

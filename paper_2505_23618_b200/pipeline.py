@@ -17,6 +17,7 @@ round trip) behind the C-ABI.  New entries:
   forward_adjusted_2d_host / ..._host         host buffers, pipelined copies
   roundtrip_adjusted_2d(_host)                forward + inverse in one kernel (device / host buffers)
   MixedBatch / mixed_forward / mixed_inverse  packed mixed-shape batches (config 3)
+  mixed_roundtrip                             both, one fused kernel per class
 Extension: base DCT-3 is accepted (the DCT-8 pre-adjustment, SURVEY.md App. A
 D3, built with design.flip_pre_adjustment); the reference raises
 ConfigurationError for it.
@@ -427,7 +428,7 @@ class MixedBatch:
             self._plan = None
 
 
-def _mixed(fn: str, batch: MixedBatch, table, x):
+def _mixed_args(batch: MixedBatch, table, x):
     t, as_np = _device.to_device(x)
     if t.dim() != 1 or t.shape[0] != batch.total_elements:
         raise ShapeError(f"expected a packed buffer of {batch.total_elements} samples")
@@ -439,6 +440,11 @@ def _mixed(fn: str, batch: MixedBatch, table, x):
         ax, m = tr.axis()
         axes[k] = ax
         keep.append(m)
+    return t, as_np, axes, keep
+
+
+def _mixed(fn: str, batch: MixedBatch, table, x):
+    t, as_np, axes, _keep = _mixed_args(batch, table, x)
     y = _device.empty_like(t)
     _lib.call(fn, batch._plan, axes, t.data_ptr(), y.data_ptr(), _device.dtype_code(t),
               _device.stream_handle())
@@ -452,6 +458,18 @@ def mixed_forward(batch: MixedBatch, table, x):
 
 def mixed_inverse(batch: MixedBatch, table, y):
     return _mixed("dctadj_mixed_inverse", batch, table, y)
+
+
+def mixed_roundtrip(batch: MixedBatch, table, x):
+    """(mixed_forward(x), mixed_inverse(of that)) with one fused kernel per class:
+    x read once, coefficients and reconstruction written once.  Bit-identical to
+    the two calls.  Returns (y, xr)."""
+    t, as_np, axes, _keep = _mixed_args(batch, table, x)
+    y = _device.empty_like(t)
+    xr = _device.empty_like(t)
+    _lib.call("dctadj_mixed_roundtrip", batch._plan, axes, t.data_ptr(), y.data_ptr(),
+              xr.data_ptr(), _device.dtype_code(t), _device.stream_handle())
+    return _device.from_device(y, as_np), _device.from_device(xr, as_np)
 
 
 # ---------------------------------------------------------------- encoder evaluation

@@ -442,6 +442,35 @@ def test_mixed_batch_matches_oracle(side, nblk):
         assert rel_err(xr[o:o + h * w].reshape(1, h, w), blk) < F32_TOL
 
 
+@pytest.mark.parametrize("side", ["pre", "post"])
+@pytest.mark.parametrize("nblk", [1, 7, 301, 5000])
+def test_mixed_roundtrip_equals_two_calls(side, nblk):
+    """Fused per-class round trip == mixed_forward then mixed_inverse, bit for bit
+    (partial super-tiles of every class), also with shuffled block offsets."""
+    from paper_2505_23618_b200 import _lib
+    rng = np.random.default_rng(100 + nblk)
+    h_index = rng.integers(0, 4, nblk)
+    v_index = rng.integers(0, 4, nblk)
+    sizes = np.array([16, 16, 32, 32])
+    areas = sizes[h_index] * sizes[v_index]
+    order = rng.permutation(nblk)
+    offs = np.zeros(nblk, np.int64)
+    offs[order] = np.concatenate([[0], np.cumsum(areas[order])[:-1]])
+    batch = pipeline.MixedBatch(offs, h_index, v_index, sizes, int(areas.sum()))
+    table = _c3_table(side)
+    axes = (_lib.Axis * 4)()
+    keep = []
+    for k, tr in enumerate(table):
+        axes[k], m = tr.axis()
+        keep.append(m)
+    assert _lib.load().dctadj_mixed_roundtrip_fused(batch._plan, axes, _lib.F32) == 1
+    x = dev(rng.standard_normal(batch.total_elements).astype(np.float32) * 20)
+    y, xr = pipeline.mixed_roundtrip(batch, table, x)
+    y2 = pipeline.mixed_forward(batch, table, x)
+    assert torch.equal(y, y2)
+    assert torch.equal(xr, pipeline.mixed_inverse(batch, table, y2))
+
+
 def test_mixed_batch_shuffled_offsets_and_errors():
     rng = np.random.default_rng(3)
     nblk = 64
