@@ -130,6 +130,12 @@ static const RtEntry kRt[] = {
     RT(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 1, false, 1),
     RTW(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, false, false, false, 1, false, 2, 2),
     RTW(float, DT_F32, 64, 64, 1, kG7F, kG7F, kG7I, kG7I, 4, 2, false, false, false, 1, false, 2, 1),
+    // y from registers (no staging tile): 6 two-warp groups x 2 stages = 12 warps/SM
+    RTW(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 6, 2, false, false, false, 1, true, 2, 3),
+    RTW(float, DT_F32, 64, 64, 1, kG7F, kG7F, kG7I, kG7I, 6, 2, false, false, false, 1, true, 2, 3),
+    // (measured, config 4, G coef/s: variant 3 post 824 / pre 530 against 797 / 600 for the two
+    //  kernels; 4 groups x 3 stages 750, one-warp packed groups 697-760)
+    RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 6, 2, false, false, false, 1, true, 2, 3),
     RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 4, 2, false, false, false, 1, false, 2, 1),
     // config 3 classes: {16,32}^2 shapes, sub-block post (DST-7 / DCT-8 share the ops) and
     // band-6 pre with DST-7 or DCT-8 per axis
