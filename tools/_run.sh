@@ -1,1 +1,5 @@
-for v in 4 5 6; do DCTADJ_RT_VARIANT=$v timeout 300 python bench.py --config c4_dst7_post --steps 10 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('v$v', round(d['value']/1e9,1), round(d['roofline']['frac'],3), d['roofline']['per_launch_ms'], d['config']['oracle_gate_rel_err'])"; done > gpurun_out/bench_c4v4.log 2>&1
+rm -f gpurun_out/configs.jsonl
+for c in c1 c2 c3_post c3_pre c4_dst7_post c4_dct8_post c4_dst7_pre c4_dct8_pre c5; do
+  timeout 600 python bench.py --config $c --steps 100 --warmup 5 --no-cpu > gpurun_out/cfg_$c.log 2>&1
+  tail -1 gpurun_out/cfg_$c.log >> gpurun_out/configs.jsonl
+done
