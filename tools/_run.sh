@@ -1,1 +1,1 @@
-timeout 600 python bench.py --config c5 --steps 100 --warmup 5 --no-cpu > gpurun_out/cfg_c5.log 2>&1
+python tools/diag/copy12.py > gpurun_out/copy12.log 2>&1
