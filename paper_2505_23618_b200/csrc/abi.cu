@@ -557,6 +557,8 @@ struct FusedArgs {
   double* err;
 };
 
+// MMA-issuer poll back-off of the fused config-5 kernel (measured, tools/prof_fused.py)
+constexpr int kFusedSpinNs = 0;
 template <int IN_MODE, int OUT_MODE, int FRC = 0, int FCC = 0>
 static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, int tiles_x,
                            const FusedArgs* fz = nullptr) {
@@ -600,6 +602,10 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   }
   int rc_s = stream_sched_counter(a.stream, &prm.sched);
   if (rc_s) return rc_s;
+  // MMA-issuer back-off between polls (DCTADJ_TC_SPIN_NS overrides the default:
+  // spin for the dense kernel, back off for the issue-bound fused one)
+  static const char* spin_env = std::getenv("DCTADJ_TC_SPIN_NS");
+  prm.spin_ns = spin_env ? std::atoi(spin_env) : (FRC != 0 ? kFusedSpinNs : 0);
   // diagnostics: DCTADJ_TC_TRACE=<file> dumps CTA 0's per-tile event clocks
   static const char* trace_file = std::getenv("DCTADJ_TC_TRACE");
   const size_t trace_bytes =

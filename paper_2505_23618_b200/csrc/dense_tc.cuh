@@ -108,6 +108,7 @@ struct DenseTcParams {
   unsigned long long* sched;  // [next, done]: dynamic tile counter, zero between launches
   double* err;     // fused: per frame [sum d^2 all, sum e^2 all, sum d^2 full rows, sum e^2 full]
   int32_t frame_h; // fused: frame height (tile rows below it are zero-padded)
+  int32_t spin_ns; // MMA issuers: back-off (ns, __nanosleep) between readiness polls; 0 = spin
 };
 constexpr int kTcTraceTiles = 128, kTcTraceEv = 8, kTcTraceCtas = 1024;
 DA_DEV unsigned long long globaltimer() {
@@ -332,9 +333,12 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
         const int g = static_cast<int>(k % NGRP);
         const uint32_t par = static_cast<uint32_t>((k / NGRP) & 1);
         bool ok;
-        while (!(ok = mbar_test(&ready[g], par))) {  // spin: try_wait's suspend adds latency
+        while (!(ok = mbar_test(&ready[g], par))) {  // poll: try_wait's suspend adds latency
           const int64_t tot = *total_k;
           if (tot >= 0 && k >= tot) break;
+          // the polling warp shares an SM sub-partition with epilogue warps: backing
+          // off returns their issue slots (the fused config-5 kernel is issue-bound)
+          if (prm.spin_ns > 0) __nanosleep(prm.spin_ns);
         }
         if (!ok) break;
         if (pass1 && prm.trace && blockIdx.x == 0 && k < kTcTraceTiles)
