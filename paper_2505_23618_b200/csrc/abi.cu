@@ -918,6 +918,28 @@ static size_t host_chunk_bytes() {
 // xrh != NULL (round trip, config 2): each chunk also runs the inverse on the
 // device-resident coefficients and copies the reconstruction back, so the
 // coefficients cross PCIe once (D2H) instead of three times.
+// Blocks per pipeline chunk: full `chunk`s, with a ramp of 1/8, 1/4, 1/2 chunks
+// at both ends of big batches so the first copy in and the last copies out
+// (which nothing overlaps) are short.  DCTADJ_HOST_RAMP=0 turns the ramp off.
+static std::vector<int64_t> host_chunk_schedule(int64_t nblk, int64_t chunk) {
+  static const bool ramp = [] {
+    const char* s = std::getenv("DCTADJ_HOST_RAMP");
+    return !(s && s[0] == '0');
+  }();
+  std::vector<int64_t> head, tail, out;
+  if (ramp && chunk >= 8 && nblk >= 4 * chunk) {
+    head = {chunk / 8, chunk / 4, chunk / 2};
+    tail = {chunk / 2, chunk / 4, chunk / 8};
+  }
+  int64_t mid = nblk;
+  for (int64_t v : head) mid -= v;
+  for (int64_t v : tail) mid -= v;
+  out = head;
+  for (int64_t b = 0; b < mid; b += chunk) out.push_back(std::min(chunk, mid - b));
+  out.insert(out.end(), tail.begin(), tail.end());
+  return out;
+}
+
 static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* xh, void* yh,
                        int64_t nblk, int dtype, bool inverse, int device, void* xrh = nullptr) {
   int rc = check_dtype(dtype);
@@ -931,7 +953,8 @@ static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x
   std::lock_guard<std::mutex> lock(hp.mu);
   const size_t blk_bytes = static_cast<size_t>(h->n) * v->n * dt_size(dtype);
   const int64_t chunk = std::max<int64_t>(1, static_cast<int64_t>(host_chunk_bytes() / blk_bytes));
-  const int64_t nchunks = (nblk + chunk - 1) / chunk;
+  const std::vector<int64_t> pieces = host_chunk_schedule(nblk, chunk);
+  const int64_t nchunks = static_cast<int64_t>(pieces.size());
   const size_t need = static_cast<size_t>(chunk) * blk_bytes;
   if (!hp.ready) {
     for (int i = 0; i < HostPipe::NSTREAM; ++i)
@@ -953,9 +976,10 @@ static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x
     hp.cap = need;
   }
   int status = ST_OK;
-  for (int64_t c = 0; c < nchunks && !status; ++c) {
+  int64_t b0 = 0;
+  for (int64_t c = 0; c < nchunks && !status; b0 += pieces[c], ++c) {
     const int k = static_cast<int>(c % HostPipe::NSTREAM);
-    const int64_t b0 = c * chunk, nb = std::min(chunk, nblk - b0);
+    const int64_t nb = pieces[c];
     const size_t off = static_cast<size_t>(b0) * blk_bytes, bytes = static_cast<size_t>(nb) * blk_bytes;
     if (cudaMemcpyAsync(hp.din[k], static_cast<const char*>(xh) + off, bytes,
                         cudaMemcpyHostToDevice, hp.st[k]) != cudaSuccess) {

@@ -1,1 +1,2 @@
-for ns in 0 20 50 100 200 400; do echo "spin $ns"; DCTADJ_TC_SPIN_NS=$ns timeout 200 python tools/prof_fused.py 10; DCTADJ_TC_SPIN_NS=$ns timeout 200 python tools/prof_dense_frames.py 10; done > gpurun_out/spin.log 2>&1
+for r in 1 0; do for c in 8 16 32; do echo "ramp $r"; DCTADJ_HOST_RAMP=$r DCTADJ_HOST_CHUNK_MB=$c timeout 120 python tools/e2e_chunks.py; done; done > gpurun_out/e2e_ramp.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k "host" >> gpurun_out/e2e_ramp.log 2>&1
