@@ -106,16 +106,17 @@ int encode_tensor_map(CUtensorMap* map, int dtype, int rank, const uint64_t* dim
 }
 
 int num_sms_cached() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[kMaxDevices];
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (!cache[dev]) {
-    int n = 0;
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (!n) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    cache[dev] = n > 0 ? n : 1;
+    n = n > 0 ? n : 1;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
-  return cache[dev];
+  return n;
 }
 
 // DCTADJ_VARIANT=k selects tuning variant k where one was built (tools/gen_instances.py
@@ -619,17 +620,9 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   auto kern = dense_tc_kernel<S, IN_MODE, OUT_MODE, FRC, FCC, NG>;
   const size_t smem = 1024 + S * 16384 + NG * 16384 + 16384 + (2 * S + 4 * NG) * 8 + (S + 1) * 8 +
                       NG * 16 * 8 + 16;
-  static int bps = 0;
-  if (!bps) {
-    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared));
-    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NTHR, smem));
-    if (bps < 1) return fail(ST_ERR_CUDA, "dense tensor-core kernel does not fit an SM");
-    bps = 1;  // the kernel allocates all 512 TMEM columns
-    if (trace_on())
-      std::fprintf(stderr, "[dctadj] dense_tc: %zu B smem, %d CTAs/SM\n", smem, bps);
-  }
+  static std::atomic<int> setup[kMaxDevices];  // per instantiation and device
+  if (!kernel_blocks_per_sm(kern, NTHR, smem, setup, "dense_tc_kernel")) return ST_ERR_CUDA;
+  const int bps = 1;  // the kernel allocates all 512 TMEM columns
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * bps;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(g.ntiles, cap)));
@@ -682,16 +675,8 @@ static int launch_dense_tc64(const LaunchArgs& a, int64_t nblocks) {
   if ((rc = stream_sched_counter(a.stream, &prm.sched))) return rc;
   auto kern = dense_tc64_kernel<S>;
   const size_t smem = 1024 + S * 32768 + NG * 32768 + 65536 + (2 * S + 4 * NG) * 8 + (S + 1) * 8 + 16;
-  static int configured = 0;
-  if (!configured) {
-    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared));
-    int bps = 0;
-    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kTc64Threads, smem));
-    if (bps < 1) return fail(ST_ERR_CUDA, "64-point tensor-core kernel does not fit an SM");
-    configured = 1;
-  }
+  static std::atomic<int> setup[kMaxDevices];  // per instantiation and device
+  if (!kernel_blocks_per_sm(kern, kTc64Threads, smem, setup, "dense_tc64_kernel")) return ST_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(g.ntiles, num_sms_cached())));
   cfg.blockDim = dim3(kTc64Threads);
@@ -1168,12 +1153,9 @@ static int launch_enc5(const void* x, void* const* outs, int64_t nblk, const dou
   }
   auto kern = enc5_kernel<T, H, W, P, NG, S>;
   const size_t smem = 1024 + static_cast<size_t>(NG) * (S + 4) * L::STAGEB + NG * S * 8;
-  static int bps = 0;
-  if (!bps) {
-    DA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, NG * 32, smem));
-    if (bps < 1) return fail(ST_ERR_CUDA, "enc5 kernel does not fit an SM");
-  }
+  static std::atomic<int> setup[kMaxDevices];  // per instantiation and device
+  const int bps = kernel_blocks_per_sm(kern, NG * 32, smem, setup, "enc5_kernel");
+  if (!bps) return ST_ERR_CUDA;
   const int64_t want = (g.ntiles + NG - 1) / NG;
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * bps;
   kern<<<static_cast<int>(std::min(want, cap)), NG * 32, smem, st>>>(in_map, om[0], om[1], om[2],

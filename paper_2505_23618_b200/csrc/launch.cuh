@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstring>
 
 #include "tile_kernel.cuh"
@@ -51,6 +52,35 @@ int encode_tensor_map(CUtensorMap* map, int dtype, int rank, const uint64_t* dim
                       void* base);
 int num_sms_cached();
 void set_last_error(const char* fmt, ...);
+
+// One-time launch setup of a kernel on the current device (dynamic shared
+// memory limit, max-shared carveout, occupancy query), cached per device in
+// the caller's per-instantiation slot array.  Function attributes are per
+// device context, so each device of a multi-GPU process configures its own;
+// racing first calls both run the (idempotent) setup.  Returns resident CTAs
+// per SM (>= 1), or 0 with the error message set.
+constexpr int kMaxDevices = 64;
+template <typename K>
+int kernel_blocks_per_sm(K kern, int threads, size_t smem, std::atomic<int> (&slot)[kMaxDevices],
+                         const char* what) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  const int cached = slot[dev].load(std::memory_order_acquire);
+  if (cached > 0) return cached;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  int nb = 0;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
+  if (e != cudaSuccess || nb < 1) {
+    set_last_error("%s setup: %s (%d CTAs/SM with %zu B shared memory)", what,
+                   cudaGetErrorString(e), nb, smem);
+    return 0;
+  }
+  slot[dev].store(nb, std::memory_order_release);
+  return nb;
+}
 
 template <typename T, int H, int W, int P, int MODE>
 int make_map(CUtensorMap* map, const void* base, const LaunchArgs& a) {
@@ -138,27 +168,9 @@ int launch_tile(const LaunchArgs& a) {
       sizeof(T) * ((RowOp::kDense ? W * W : 0) + (ColOp::kDense ? H * H : 0));
   const size_t smem = 1024 + static_cast<size_t>(NG) * S * L::STAGEB + NG * S * 8 + dense_bytes;
 
-  static int configured = 0;  // per instantiation
-  static int blocks_per_sm = 1;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) {
-      set_last_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-      return ST_ERR_CUDA;
-    }
-    int nb = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NG * NW * 32, smem);
-    if (e != cudaSuccess || nb < 1) {
-      set_last_error("occupancy query failed (%s, %d blocks)", cudaGetErrorString(e), nb);
-      return ST_ERR_CUDA;
-    }
-    blocks_per_sm = nb;
-    configured = 1;
-  }
+  static std::atomic<int> setup[kMaxDevices];  // per instantiation and device
+  const int blocks_per_sm = kernel_blocks_per_sm(kern, NG * NW * 32, smem, setup, "tile_kernel");
+  if (!blocks_per_sm) return ST_ERR_CUDA;
   const int64_t want = (g.ntiles + NG - 1) / NG;
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * blocks_per_sm;
   const int grid = static_cast<int>(want < cap ? want : cap);

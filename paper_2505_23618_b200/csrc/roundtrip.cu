@@ -45,22 +45,9 @@ int launch_roundtrip(const RtArgs& a) {
   auto kern =
       roundtrip_kernel<T, H, W, P, RCF, CCF, RCI, CCI, NG, S, PRF, PC, PRI, MINB, YSTG, NW, CH, MODE>;
   const size_t smem = 1024 + static_cast<size_t>(NG) * (YSTG ? S : S + 1) * L::STAGEB + NG * S * 8;
-  static int blocks_per_sm = 0;  // per instantiation
-  if (!blocks_per_sm) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    int nb = 0;
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NG * NW * 32, smem);
-    if (e != cudaSuccess || nb < 1) {
-      set_last_error("roundtrip_kernel setup: %s (%d blocks/SM)", cudaGetErrorString(e), nb);
-      return ST_ERR_CUDA;
-    }
-    blocks_per_sm = nb;
-  }
+  static std::atomic<int> setup[kMaxDevices];  // per instantiation and device
+  const int blocks_per_sm = kernel_blocks_per_sm(kern, NG * NW * 32, smem, setup, "roundtrip_kernel");
+  if (!blocks_per_sm) return ST_ERR_CUDA;
   const int64_t want = (g.ntiles + NG - 1) / NG;
   const int64_t cap = static_cast<int64_t>(num_sms_cached()) * blocks_per_sm;
   cudaLaunchConfig_t cfg = {};

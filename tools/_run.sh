@@ -1,2 +1,3 @@
-for r in 1 0; do for c in 8 16 32; do echo "ramp $r"; DCTADJ_HOST_RAMP=$r DCTADJ_HOST_CHUNK_MB=$c timeout 120 python tools/e2e_chunks.py; done; done > gpurun_out/e2e_ramp.log 2>&1
-timeout 600 python -m pytest tests -m gpu -x -q -k "host" >> gpurun_out/e2e_ramp.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$? >> gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1
