@@ -211,6 +211,21 @@ int32_t dctadj_version(void);
 /* number of tile_kernel instantiations compiled into this library */
 int32_t dctadj_kernel_count(void);
 
+/* ---- adjustment designer (offline) ----
+ * The reference's cyclic coordinate descent over the angles of a rotation
+ * skeleton (design.py:377-543, the optimize_adjustment path without the
+ * sparsity penalty), every restart in its own CTA.  Host arrays in / out:
+ * base, desired: n x n row-major (n <= 64); weights: n; side 0 = pre
+ * (H = B A), 1 = post (H = A B); rotation t acts on (rp[t], rq[t]);
+ * theta0: restarts x m start angles.  Out: theta (restarts x m), trace
+ * (restarts x (max_sweeps + 1) objectives; entry k after sweep k), sweeps
+ * (trace length - 1) and converged flags per restart.  Blocks until done. */
+int dctadj_design_cd(int32_t n, const double* base, const double* desired,
+                     const double* weights, int32_t side, int32_t m, const int32_t* rp,
+                     const int32_t* rq, int32_t restarts, const double* theta0,
+                     int32_t max_sweeps, double tol, double* theta_out, double* trace_out,
+                     int32_t* sweeps_out, int32_t* converged_out, int32_t device);
+
 #ifdef __cplusplus
 }
 #endif

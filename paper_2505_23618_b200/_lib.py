@@ -82,6 +82,8 @@ SIGNATURES = {
     "dctadj_mixed_inverse": [_P, _AP, _P, _P, _I32, _P],
     "dctadj_mixed_roundtrip": [_P, _AP, _P, _P, _P, _I32, _P],
     "dctadj_mixed_roundtrip_fused": [_P, _AP, _I32],
+    "dctadj_design_cd": [_I32, _P, _P, _P, _I32, _I32, _P, _P, _I32, _P, _I32, ctypes.c_double,
+                         _P, _P, _P, _P, _I32],
     "dctadj_mixed_destroy": [_P],
     "dctadj_status_string": [_I32],
     "dctadj_last_error": [],

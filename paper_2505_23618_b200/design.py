@@ -1,8 +1,9 @@
 """Adjustment parameter records (host side).
 
 The adjustment *designer* (the reference's coordinate-descent optimizer,
-design.py:333-613) is offline and out of scope; designed adjustments arrive as
-files in the reference's text format (matio.py) -- see adjustments/.  This
+design.py:333-613) is offline: designed adjustments arrive as files in the
+reference's text format (matio.py) -- see adjustments/ -- and designer.py runs
+the optimizer itself on the GPU.  This
 module keeps the records and structural helpers the data path needs, with the
 reference's semantics:
 

@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$? >> gpurun_out/smoke.log
-timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1
+timeout 600 python -m pytest tests/test_designer.py -q > gpurun_out/pytest_des.log 2>&1; echo pytest=$? >> gpurun_out/pytest_des.log
+timeout 900 python tools/design_gpu.py > gpurun_out/design_gpu.log 2>&1
