@@ -8,9 +8,9 @@
 // each angle step is
 //   8 length-N reductions + 2 matrix-vector products (the degree-2 trig
 //   polynomial of the weighted error in (cos, sin), design.py:442-475)
-//   -> the 33-point grid, golden-section refinement to 1e-12 and the
-//      {0, theta_old} candidates with the reference's tie rule
-//      (design.py:333-374), on one thread, in the reference's order
+//   -> the 33-point grid (one lane per point), golden-section refinement to
+//      1e-12 and the {0, theta_old} candidates with the reference's tie rule
+//      (design.py:333-374) in the reference's order
 //   -> rank-2 updates of E and A (design.py:503-510)
 //   -> strip the next rotation from UA (UW), apply this one to VA (VW)
 //      (design.py:515-523).
@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(kThreads) cd_kernel(const Args g) {
         if (lane == 0) red[warp] = acc;
       }
       __syncthreads();
-      if (tid == 0) {
+      if (tid < 32) {  // warp 0: the 1-D minimisation (design.py:352-374)
+        const int lane = tid;
         const double suu_pp = red[0], suu_qq = red[1], suu_pq = red[2];
         const double svv_pp = red[3], svv_qq = red[4], svv_pq = red[5];
         const double we_p = red[6], we_q = red[7];
@@ -253,37 +254,54 @@ __global__ void __launch_bounds__(kThreads) cd_kernel(const Args g) {
         f.bq = we_q - co * f.apq - so * f.aqq;
         f.cst = (wobj - 2 * co * we_p - 2 * so * we_q + co * co * f.app + so * so * f.aqq +
                  2 * co * so * f.apq);
-        // grid argmin (first minimum, as np.argmin), bracket, golden section
+        // the 33 grid values, one (lane 0: two) per lane; argmin keeps the first
+        // minimum like np.argmin.  Lanes 1 / 2 also evaluate the two candidates.
         const double step = 2 * kHalfPi / (kGrid - 1);
-        int kbest = 0;
-        double gbest = 0.0;
-        for (int k = 0; k < kGrid; ++k) {
-          const double gv = f.at(-kHalfPi + k * step);
-          if (k == 0 || gv < gbest) {
+        double gbest = f.at(-kHalfPi + lane * step);
+        int kbest = lane;
+        if (lane == 0) {
+          const double g32 = f.at(-kHalfPi + (kGrid - 1) * step);
+          if (g32 < gbest) {
+            gbest = g32;
+            kbest = kGrid - 1;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double gv = __shfl_xor_sync(0xffffffffu, gbest, o);
+          const int gk = __shfl_xor_sync(0xffffffffu, kbest, o);
+          if (gv < gbest || (gv == gbest && gk < kbest)) {
             gbest = gv;
-            kbest = k;
+            kbest = gk;
           }
         }
-        const double gk = -kHalfPi + kbest * step;
-        const double lo = fmax(-kHalfPi, gk - step), hi = fmin(kHalfPi, gk + step);
-        double t_best = golden_min(f, lo, hi);
-        double f_best = f.at(t_best);
-        const double cands[2] = {0.0, th[t]};
-        for (int ci = 0; ci < 2; ++ci) {
-          const double fc = f.at(cands[ci]);
-          const double tie = 1e-15 * (1.0 + fabs(f_best));
-          if (fc < f_best - tie || (fabs(fc - f_best) <= tie && fabs(cands[ci]) < fabs(t_best))) {
-            f_best = fc;
-            t_best = cands[ci];
+        const double th_old = th[t];
+        const double fcand = lane == 1 ? f.at(0.0) : lane == 2 ? f.at(th_old) : 0.0;
+        const double fc0 = __shfl_sync(0xffffffffu, fcand, 1);
+        const double fco = __shfl_sync(0xffffffffu, fcand, 2);
+        if (lane == 0) {
+          const double gk = -kHalfPi + kbest * step;
+          const double lo = fmax(-kHalfPi, gk - step), hi = fmin(kHalfPi, gk + step);
+          double t_best = golden_min(f, lo, hi);
+          double f_best = f.at(t_best);
+          const double cands[2] = {0.0, th_old}, fcs[2] = {fc0, fco};
+          for (int ci = 0; ci < 2; ++ci) {
+            const double fc = fcs[ci];
+            const double tie = 1e-15 * (1.0 + fabs(f_best));
+            if (fc < f_best - tie ||
+                (fabs(fc - f_best) <= tie && fabs(cands[ci]) < fabs(t_best))) {
+              f_best = fc;
+              t_best = cands[ci];
+            }
           }
+          double sn, cn;
+          sincos(t_best, &sn, &cn);
+          sc[0] = cn;
+          sc[1] = sn;
+          sc[2] = f_best;
+          sc[3] = f(cn, sn);  // the new weighted objective
+          th[t] = t_best;
         }
-        double sn, cn;
-        sincos(t_best, &sn, &cn);
-        sc[0] = cn;
-        sc[1] = sn;
-        sc[2] = f_best;
-        sc[3] = f(cn, sn);  // the new weighted objective
-        th[t] = t_best;
       }
       __syncthreads();
       const double cn = sc[0], sn = sc[1], dc = cn - co, ds = sn - so;
