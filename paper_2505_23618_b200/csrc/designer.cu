@@ -95,27 +95,64 @@ struct Quad {  // the weighted error as a degree-2 polynomial in (cos, sin)
   }
 };
 
-// reference _golden_min (design.py:333-347)
-__device__ double golden_min(const Quad& f, double lo, double hi) {
-  double a = lo, b = hi;
-  double x1 = b - kGolden * (b - a), x2 = a + kGolden * (b - a);
-  double f1 = f.at(x1), f2 = f.at(x2);
-  while (b - a > kAngleTol) {
-    if (f1 <= f2) {
+// reference _golden_min (design.py:333-347) on a whole warp, speculatively:
+// the points a golden-section
+// step creates depend only on the earlier steps' comparisons, so each round
+// evaluates every point of the next 5 steps' decision tree at once (31 lanes,
+// heap order: node k's children are 2k (f1 <= f2: the bracket keeps [a, x2])
+// and 2k+1), then replays the 5 comparisons on the values.  Points, values and
+// decisions are the serial ones bit for bit; the dependent sincos chain drops
+// from ~56 to ~12 links.  All 32 lanes call; every lane returns the result.
+struct GoldenState {
+  double a, b, x1, x2;
+  // one step taking branch `keep_left` (f1 <= f2); returns the new point
+  __device__ double step(bool keep_left) {
+    if (keep_left) {
       b = x2;
       x2 = x1;
-      f2 = f1;
       x1 = b - kGolden * (b - a);
-      f1 = f.at(x1);
-    } else {
-      a = x1;
-      x1 = x2;
-      f1 = f2;
-      x2 = a + kGolden * (b - a);
-      f2 = f.at(x2);
+      return x1;
+    }
+    a = x1;
+    x1 = x2;
+    x2 = a + kGolden * (b - a);
+    return x2;
+  }
+};
+
+__device__ double golden_min_warp(const Quad& f, double lo, double hi, int lane) {
+  constexpr int kDepth = 5;  // 2^5 - 1 = 31 tree nodes per round
+  GoldenState st{lo, hi, 0.0, 0.0};
+  st.x1 = hi - kGolden * (hi - lo);
+  st.x2 = lo + kGolden * (hi - lo);
+  const double fx = f.at(lane == 0 ? st.x1 : st.x2);
+  double f1 = __shfl_sync(0xffffffffu, fx, 0), f2 = __shfl_sync(0xffffffffu, fx, 1);
+  while (st.b - st.a > kAngleTol) {
+    // lane L evaluates tree node L + 1: the first decision is known, the next
+    // ones are the bits of the node number below its leading one
+    const int node = lane + 1;
+    const int depth = 31 - __clz(node);  // node's level - 1
+    GoldenState sp = st;
+    double pt = sp.step(f1 <= f2);
+    for (int d = depth - 1; d >= 0; --d) pt = sp.step(((node >> d) & 1) == 0);
+    const double val = lane < 31 ? f.at(pt) : 0.0;
+    // replay the real path through the tree
+    int k = 1;
+    for (int lvl = 0; lvl < kDepth && st.b - st.a > kAngleTol; ++lvl) {
+      const bool keep_left = f1 <= f2;
+      if (lvl > 0) k = 2 * k + (keep_left ? 0 : 1);
+      st.step(keep_left);
+      const double v = __shfl_sync(0xffffffffu, val, k - 1);
+      if (keep_left) {
+        f2 = f1;
+        f1 = v;
+      } else {
+        f1 = f2;
+        f2 = v;
+      }
     }
   }
-  return 0.5 * (a + b);
+  return 0.5 * (st.a + st.b);
 }
 
 // one CTA = one restart
@@ -279,10 +316,11 @@ __global__ void __launch_bounds__(kThreads) cd_kernel(const Args g) {
         const double fcand = lane == 1 ? f.at(0.0) : lane == 2 ? f.at(th_old) : 0.0;
         const double fc0 = __shfl_sync(0xffffffffu, fcand, 1);
         const double fco = __shfl_sync(0xffffffffu, fcand, 2);
+        const double gk = -kHalfPi + kbest * step;
+        const double lo = fmax(-kHalfPi, gk - step), hi = fmin(kHalfPi, gk + step);
+        const double t_gold = golden_min_warp(f, lo, hi, lane);
         if (lane == 0) {
-          const double gk = -kHalfPi + kbest * step;
-          const double lo = fmax(-kHalfPi, gk - step), hi = fmin(kHalfPi, gk + step);
-          double t_best = golden_min(f, lo, hi);
+          double t_best = t_gold;
           double f_best = f.at(t_best);
           const double cands[2] = {0.0, th_old}, fcs[2] = {fc0, fco};
           for (int ci = 0; ci < 2; ++ci) {
