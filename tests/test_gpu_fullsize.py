@@ -63,3 +63,40 @@ def test_c5_full_size_frames():
     assert 0.05 < e[0] / e[1] < 0.09  # ~7 % of the energy (config 5)
     # energy: padded tile rows are zero, so the adjusted coefficients carry the frames' energy
     assert abs(_energy(w.y) / _energy(w.frames) - 1) < TOL
+
+
+def test_c2_full_size_fused_round_trip():
+    """The bench step itself (65,536 x 32x32 fp32 integer residuals, one fused
+    round-trip kernel): x' recovers x exactly after rounding (D7 iii), and the
+    coefficients / reconstruction equal the two-kernel schedule bit for bit."""
+    import bench
+    w = bench.Uniform("c2", 0, fused_roundtrip=True)
+    assert [n for n, _ in w.launches] == ["roundtrip_2d"]
+    for _, fn in w.launches:
+        fn()
+    torch.cuda.synchronize()
+    y, xr = w.y.clone(), w.xr.clone()
+    assert torch.equal(torch.round(xr), w.x)
+    assert abs(_energy(y) / _energy(w.x) - 1) < TOL
+    for _, fn in w.two_kernel:
+        fn()
+    torch.cuda.synchronize()
+    assert torch.equal(y, w.y) and torch.equal(xr, w.xr)
+    assert w.gate() < TOL
+
+
+@pytest.mark.parametrize("side", ["pre", "post"])
+def test_c3_full_size_fused_round_trip(side):
+    import bench
+    w = bench.Mixed(side, 0, fused_roundtrip=True)  # 1,048,576 blocks, one kernel per class
+    assert [n for n, _ in w.launches] == ["mixed_roundtrip"]
+    for _, fn in w.launches:
+        fn()
+    torch.cuda.synchronize()
+    y, xr = w.y.clone(), w.xr.clone()
+    err = (xr - w.x).abs().max().item() / w.x.abs().max().item()
+    assert err < TOL
+    for _, fn in w.two_kernel:
+        fn()
+    torch.cuda.synchronize()
+    assert torch.equal(y, w.y) and torch.equal(xr, w.xr)
