@@ -279,6 +279,21 @@ def test_roundtrip_c2_integer_exact_and_fp64(golden):
     assert rel_err(xr64.cpu().numpy(), x64.cpu().numpy()) < F64_TOL
 
 
+def test_roundtrip_empty_and_bad_shapes():
+    t = pipeline.make_adjusted_transform(_rt_transforms()["dct8_post"])
+    y, xr = pipeline.roundtrip_adjusted_2d(t, t, torch.empty(0, 32, 32, device="cuda"))
+    assert y.shape == (0, 32, 32) and xr.shape == (0, 32, 32)
+    yh, xh = pipeline.roundtrip_adjusted_2d_host(t, t, np.zeros((0, 32, 32), np.float32))
+    assert yh.shape == (0, 32, 32) and xh.shape == (0, 32, 32)
+    with pytest.raises(ShapeError):
+        pipeline.roundtrip_adjusted_2d(t, t, torch.zeros(4, 32, 16, device="cuda"))
+    with pytest.raises(ShapeError):
+        pipeline.roundtrip_adjusted_2d_host(t, t, np.zeros((4, 16, 32), np.float32))
+    batch = pipeline.MixedBatch.packed(np.zeros(0, np.int64), np.zeros(0, np.int64), [16, 16, 32, 32])
+    y, xr = pipeline.mixed_roundtrip(batch, _c3_table("post"), torch.empty(0, device="cuda"))
+    assert y.numel() == 0 and xr.numel() == 0
+
+
 def test_roundtrip_in_place_and_alias_rule():
     """xr may alias x (C-ABI); y aliasing xr is rejected before any work."""
     import ctypes
