@@ -877,7 +877,7 @@ static int run_roundtrip(const dctadj_axis* h, const dctadj_axis* v, const void*
 // (PCIe is full duplex).  Streams and staging buffers persist per device
 // (one pipeline at a time per device; concurrent host calls serialise).
 struct HostPipe {
-  static constexpr int NSTREAM = 4;
+  static constexpr int NSTREAM = 8;  // capacity; host_streams() are used
   std::mutex mu;
   bool ready = false;
   cudaStream_t st[NSTREAM] = {};
@@ -889,6 +889,16 @@ struct HostPipe {
 static HostPipe& host_pipe(int device) {
   static HostPipe pipes[64];
   return pipes[(device >= 0 && device < 64) ? device : 0];
+}
+
+// streams in the host pipeline (DCTADJ_HOST_STREAMS, 2..8; default 4)
+static int host_streams() {
+  static const int v = [] {
+    const char* s = std::getenv("DCTADJ_HOST_STREAMS");
+    const int n = s ? std::atoi(s) : 4;
+    return n < 2 ? 2 : n > 8 ? 8 : n;
+  }();
+  return v;
 }
 
 static size_t host_chunk_bytes() {
@@ -954,7 +964,7 @@ static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x
       hp.din[i] = hp.dout[i] = nullptr;
     }
     hp.cap = 0;
-    for (int i = 0; i < HostPipe::NSTREAM; ++i) {
+    for (int i = 0; i < host_streams(); ++i) {
       DA_CUDA(cudaMalloc(&hp.din[i], need));
       DA_CUDA(cudaMalloc(&hp.dout[i], need));
     }
@@ -963,7 +973,7 @@ static int run_2d_host(const dctadj_axis* h, const dctadj_axis* v, const void* x
   int status = ST_OK;
   int64_t b0 = 0;
   for (int64_t c = 0; c < nchunks && !status; b0 += pieces[c], ++c) {
-    const int k = static_cast<int>(c % HostPipe::NSTREAM);
+    const int k = static_cast<int>(c % host_streams());
     const int64_t nb = pieces[c];
     const size_t off = static_cast<size_t>(b0) * blk_bytes, bytes = static_cast<size_t>(nb) * blk_bytes;
     if (cudaMemcpyAsync(hp.din[k], static_cast<const char*>(xh) + off, bytes,
