@@ -1,5 +1,5 @@
 #!/bin/bash
-# config-4 band-pre timing per tuning variant (0 = default, 11-14 = split64 kernels)
+# config-4 band-pre timing per tuning variant (DCTADJ_VARIANT; 0 = default, 1-6 = tools/gen_instances.py EXPERIMENT)
 for c in c4_dst7_pre c4_dct8_pre; do
   for v in "$@"; do
     DCTADJ_VARIANT=$v timeout 200 python bench.py --config $c --no-cpu --steps 20 --warmup 3 > gpurun_out/v.log 2>&1
