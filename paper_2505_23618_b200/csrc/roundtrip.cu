@@ -106,6 +106,7 @@ static const RtEntry kRt[] = {
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 4, false, 5),
     RT(float, DT_F32, 32, 32, 4, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 6),
     // (L2 evict-first hints on the loads, the stores or both: no change, 137.9-139.1 us)
+    // (16 KB super-tiles shared by two warps, 2 groups x (2 + 1): 156.6-160.2 us)
     // y stored from registers (no staging tile; measured slower: 0.83 vs 0.90)
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 3, true, 7),
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 6, true, 8),
