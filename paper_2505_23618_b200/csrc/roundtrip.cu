@@ -86,11 +86,12 @@ constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS, 6);
    &launch_roundtrip<float, H, W, 2048 / (H * W), RF, CF, RI, CI, NG, 2, true, true, PRI, MINB,    \
                      false, 1, 0, MODE_GATHER>}
 // default + variants 1, 2: (4 warps, 128 registers), (4 warps, 255), (3 warps, 168); the
-// band-6 pre classes default to the 255-register build (measured 752 vs 735 G coef/s)
+// band-6 pre classes default to the 255-register build with scalar inverse rows
+// (measured 762 G coef/s; packed inverse rows 752 / 128 registers 735)
 #define RTG(H, W, RF, CF, RI, CI, PRI, VAR) RTGV(H, W, RF, CF, RI, CI, PRI, 4, 4, VAR), \
   RTGV(H, W, RF, CF, RI, CI, PRI, 4, 2, VAR + 1), RTGV(H, W, RF, CF, RI, CI, PRI, 3, 3, VAR + 2)
-#define RTGP(H, W, RF, CF, RI, CI) RTGV(H, W, RF, CF, RI, CI, true, 4, 2, 0), \
-  RTGV(H, W, RF, CF, RI, CI, true, 4, 4, 1), RTGV(H, W, RF, CF, RI, CI, true, 3, 3, 2)
+#define RTGP(H, W, RF, CF, RI, CI) RTGV(H, W, RF, CF, RI, CI, false, 4, 2, 0), \
+  RTGV(H, W, RF, CF, RI, CI, true, 4, 4, 1), RTGV(H, W, RF, CF, RI, CI, true, 4, 2, 2)
 #define RT(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, VAR) \
   RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, 1, VAR)
 
@@ -110,11 +111,13 @@ static const RtEntry kRt[] = {
     // y stored from registers (no staging tile; measured slower: 0.83 vs 0.90)
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 3, true, 7),
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 6, true, 8),
-    // 32x32 fp32, band-6 pre (DST-7 / DCT-8 via the DCT-3 base)
-    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 4, false, 0),
-    RT(float, DT_F32, 32, 32, 2, kG8F, kG8F, kG8I, kG8I, 4, 2, true, true, true, 4, false, 0),
+    // 32x32 fp32, band-6 pre (DST-7 / DCT-8 via the DCT-3 base): scalar inverse rows,
+    // 255-register budget (177 us per 65,536 blocks; packed inverse rows 188-193 us,
+    // y from registers at 12 warps/SM 177 us, 3 warps 219 us)
+    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, false, 2, false, 0),
+    RT(float, DT_F32, 32, 32, 2, kG8F, kG8F, kG8I, kG8I, 4, 2, true, true, false, 2, false, 0),
     RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 2, false, 1),
-    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 3, 2, true, true, true, 3, false, 2),
+    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 3, true, 3),
     // 64x64 fp32 (config 4): built as tuning variants only -- measured slower than
     // the two tile kernels (shared memory holds 4-8 warps/SM at 16 KB per block
     // and 3 buffers per group: sub-8 post 0.52-0.62, band-6 pre 0.44 of the copy
