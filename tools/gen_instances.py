@@ -71,11 +71,12 @@ def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False
             # (the packed 64-column pass needs ~200 registers; measured faster)
             return p, 6, 2, ("NW", 2, 0)
     if two_d and dtype == "double" and (h, w) == (32, 32):
-        # fp64 32x32 (config 1): two warps per 2-block super-tile, two stages, and a
-        # 170-register cap (launch bounds: 6 CTAs/SM) -> 12 warps/SM, no spills.
-        # Measured 14.3 us vs 16.9 us per 4,096-block forward (4 x 1 warp, 3 stages,
-        # 255 registers, 8 warps/SM); profiles/r01_tuning.md
-        return 2, 1, 2, ("NW", 2, 0x60)
+        # fp64 32x32 (config 1): one-warp CTAs, one block per stage, two stages, 12
+        # CTAs/SM (launch bounds) -> 12 warps/SM, no spills; small CTAs let the next
+        # launch's CTAs become resident as these retire.  Measured 13.9 us per
+        # 4,096-block forward vs 14.2 (two-warp groups on 2-block super-tiles, 6
+        # CTAs/SM) and 16.9 (4 x 1 warp, 3 stages, 8 warps/SM); profiles/r01_tuning.md
+        return 1, 1, 2, ("NW", 1, 0xC0)
     if stage <= 2048:
         ng, s = 8, 4
     elif stage <= 4096:
@@ -150,7 +151,8 @@ EXPERIMENT = {
                          (2, 1, 3, False, False, 0, 2), (2, 1, 2, False, False, 0x60, 2),
                          (2, 1, 3, False, False, 0x50, 2), (4, 1, 3, False, False, 0, 4),
                          (4, 1, 2, False, False, 0x30, 4), (2, 1, 4, False, False, 0x40, 2),
-                         (1, 6, 2, False, False, 0, 1), (2, 1, 5, False, False, 0, 2)],
+                         (1, 6, 2, False, False, 0, 1), (2, 1, 5, False, False, 0, 2),
+                         (2, 1, 2, False, False, 0x60, 2), (1, 1, 3, False, False, 0x80, 1)],
     ("float", 32, 32): [(4, 2, 3, True, True, 0), (2, 4, 4, True, True, 0), (4, 2, 3, False, True, 0),
                (2, 4, 4, False, True, 0)],
     ("float", 64, 64): [(1, 6, 2, False, False, 0, 2), (1, 4, 3, False, False, 0, 2),
