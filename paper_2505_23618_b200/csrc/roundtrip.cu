@@ -108,6 +108,7 @@ static const RtEntry kRt[] = {
     RT(float, DT_F32, 32, 32, 4, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 6),
     // (L2 evict-first hints on the loads, the stores or both: no change, 137.9-139.1 us)
     // (16 KB super-tiles shared by two warps, 2 groups x (2 + 1): 156.6-160.2 us)
+    // (one-warp CTAs, 8 per SM: 140.6 us sub-8 post, 183.7 us band-6 pre -- no gain here)
     // y stored from registers (no staging tile; measured slower: 0.83 vs 0.90)
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 3, true, 7),
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 6, true, 8),
