@@ -85,13 +85,16 @@ constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS, 6);
   {DT_F32, H, W, RF, CF, RI, CI, MODE_GATHER, VAR,                                               \
    &launch_roundtrip<float, H, W, 2048 / (H * W), RF, CF, RI, CI, NG, 2, true, true, PRI, MINB,    \
                      false, 1, 0, MODE_GATHER>}
-// default + variants 1, 2: (4 warps, 128 registers), (4 warps, 255), (3 warps, 168); the
-// band-6 pre classes default to the 255-register build with scalar inverse rows
-// (measured 762 G coef/s; packed inverse rows 752 / 128 registers 735)
-#define RTG(H, W, RF, CF, RI, CI, PRI, VAR) RTGV(H, W, RF, CF, RI, CI, PRI, 4, 4, VAR), \
-  RTGV(H, W, RF, CF, RI, CI, PRI, 4, 2, VAR + 1), RTGV(H, W, RF, CF, RI, CI, PRI, 3, 3, VAR + 2)
+// sub-8 post classes: default one-warp CTAs, 8 per SM (956 G coef/s on config 3),
+// variants 1-4: 4 warps at 255 registers, 3 warps, 2 warps, 4 warps at 128 (941-944);
+// band-6 pre classes: 4 warps at 255 registers with scalar inverse rows (762;
+// packed inverse rows 752, 128 registers 735, 2- / 1-warp CTAs 761-764)
+#define RTG(H, W, RF, CF, RI, CI, PRI, VAR) RTGV(H, W, RF, CF, RI, CI, PRI, 1, 8, VAR), \
+  RTGV(H, W, RF, CF, RI, CI, PRI, 4, 2, VAR + 1), RTGV(H, W, RF, CF, RI, CI, PRI, 3, 3, VAR + 2), \
+  RTGV(H, W, RF, CF, RI, CI, PRI, 2, 4, VAR + 3), RTGV(H, W, RF, CF, RI, CI, PRI, 4, 4, VAR + 4)
 #define RTGP(H, W, RF, CF, RI, CI) RTGV(H, W, RF, CF, RI, CI, false, 4, 2, 0), \
-  RTGV(H, W, RF, CF, RI, CI, true, 4, 4, 1), RTGV(H, W, RF, CF, RI, CI, true, 4, 2, 2)
+  RTGV(H, W, RF, CF, RI, CI, true, 4, 4, 1), RTGV(H, W, RF, CF, RI, CI, true, 4, 2, 2), \
+  RTGV(H, W, RF, CF, RI, CI, false, 2, 4, 3), RTGV(H, W, RF, CF, RI, CI, false, 1, 8, 4)
 #define RT(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, VAR) \
   RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, 1, VAR)
 
