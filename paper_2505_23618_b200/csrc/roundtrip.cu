@@ -135,6 +135,7 @@ static const RtEntry kRt[] = {
     // (measured, config 4, G coef/s: variant 3 post 824 / pre 530 against 797 / 600 for the two
     //  kernels; 4 groups x 3 stages 750, one-warp packed groups 697-760)
     RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 6, 2, false, false, false, 1, true, 2, 3),
+    // (one two-warp group per CTA, 6 CTAs/SM: post 799, pre 572 -- no gain)
     RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 4, 2, false, false, false, 1, false, 2, 1),
     // config 3 classes: {16,32}^2 shapes, sub-block post (DST-7 / DCT-8 share the ops) and
     // band-6 pre with DST-7 or DCT-8 per axis
