@@ -155,7 +155,8 @@ int dctadj_inverse_frames(const dctadj_axis* h, const dctadj_axis* v, const void
  * (Givens) pre adjustment on both axes, dense exact axes and width a multiple of
  * 128 runs as ONE tensor-core kernel that reads the frames once
  * (csrc/dense_tc.cuh, FUSED); anything else runs the two frame transforms and a
- * reduction.  Replaces the reference's two transform calls plus its error sum
+ * reduction.  The error sums are defined on 32x32 tiles: other block sizes
+ * with err != NULL return DCTADJ_ERR_UNSUPPORTED (with err = NULL they run).  Replaces the reference's two transform calls plus its error sum
  * (reference pipeline.py:176-199). */
 int dctadj_forward_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dctadj_axis* eh,
                                 const dctadj_axis* ev, const void* frames, void* coefs,
@@ -210,6 +211,12 @@ const char* dctadj_last_error(void);
 int32_t dctadj_version(void);
 /* number of tile_kernel instantiations compiled into this library */
 int32_t dctadj_kernel_count(void);
+/* the device cache of dense matrices (composites, exact comparison transforms):
+ * entries held and entries pinned by calls still in flight (0 between calls) */
+int dctadj_dense_cache_state(int32_t* entries, int32_t* pinned);
+/* 1 when the library was built with DCTADJ_TUNING=1 (measured-slower tuning
+ * variants selectable by DCTADJ_VARIANT / DCTADJ_RT_VARIANT), else 0 */
+int32_t dctadj_tuning_build(void);
 
 /* ---- adjustment designer (offline) ----
  * The reference's cyclic coordinate descent over the angles of a rotation

@@ -89,6 +89,8 @@ SIGNATURES = {
     "dctadj_last_error": [],
     "dctadj_version": [],
     "dctadj_kernel_count": [],
+    "dctadj_dense_cache_state": [ctypes.POINTER(_I32), ctypes.POINTER(_I32)],
+    "dctadj_tuning_build": [],
 }
 
 _lib = None

@@ -370,19 +370,27 @@ static std::vector<unsigned char> to_dtype(const std::vector<double>& v, int dty
   return out;
 }
 
-// stream-ordered device copy of a dense matrix; freed with free_dense after use
 // Dense matrices (composites, the exact comparison transforms) are cached on the
 // device by content: a call stream-orders nothing and allocates nothing once the
 // matrix has been seen.  A miss uploads synchronously, so the copy is visible to
-// every stream; entries live until the cache overflows (then the oldest goes,
-// after a device synchronisation inside cudaFree).
+// every stream.  upload_dense PINS the entry it returns; the caller unpins it
+// (release_dense, done by ~Launch / Launch::reset) once its kernels are enqueued,
+// so an entry is never evicted between lookup and launch -- by this call's own
+// second upload or by another thread.  When the cache is full the least
+// recently used unpinned entry of this device is freed after a device-wide
+// synchronisation (kernels enqueued earlier may still read it); if every entry
+// is pinned the cache grows instead.
 struct DenseCacheEntry {
   int device, dtype;
   std::vector<double> m;
   void* ptr;
+  int pins;
+  uint64_t last_use;
 };
 static std::mutex g_dense_mu;
 static std::vector<DenseCacheEntry> g_dense_cache;
+static uint64_t g_dense_tick = 0;
+static constexpr size_t kDenseCacheSlots = 64;
 
 static int upload_dense(const AxisPlan& p, int dtype, cudaStream_t st, void** dev) {
   (void)st;
@@ -393,28 +401,73 @@ static int upload_dense(const AxisPlan& p, int dtype, cudaStream_t st, void** de
   std::lock_guard<std::mutex> lk(g_dense_mu);
   for (auto& e : g_dense_cache)
     if (e.device == device && e.dtype == dtype && e.m == p.dense) {
+      ++e.pins;
+      e.last_use = ++g_dense_tick;
       *dev = e.ptr;
       return ST_OK;
     }
-  if (g_dense_cache.size() >= 64) {
-    DA_CUDA(cudaFree(g_dense_cache.front().ptr));
-    g_dense_cache.erase(g_dense_cache.begin());
+  if (g_dense_cache.size() >= kDenseCacheSlots) {
+    size_t victim = g_dense_cache.size();
+    for (size_t i = 0; i < g_dense_cache.size(); ++i) {
+      const auto& e = g_dense_cache[i];
+      if (e.pins == 0 && e.device == device &&
+          (victim == g_dense_cache.size() || e.last_use < g_dense_cache[victim].last_use))
+        victim = i;
+    }
+    if (victim < g_dense_cache.size()) {
+      DA_CUDA(cudaDeviceSynchronize());  // kernels enqueued before may still read it
+      DA_CUDA(cudaFree(g_dense_cache[victim].ptr));
+      g_dense_cache.erase(g_dense_cache.begin() + static_cast<std::ptrdiff_t>(victim));
+    }
   }
   std::vector<unsigned char> host = to_dtype(p.dense, dtype);
   void* ptr = nullptr;
   DA_CUDA(cudaMalloc(&ptr, host.size()));
   DA_CUDA(cudaMemcpy(ptr, host.data(), host.size(), cudaMemcpyHostToDevice));
-  g_dense_cache.push_back({device, dtype, p.dense, ptr});
+  g_dense_cache.push_back({device, dtype, p.dense, ptr, 1, ++g_dense_tick});
   *dev = ptr;
   return ST_OK;
+}
+
+// unpin an entry returned by upload_dense (NULL: no-op)
+static void release_dense(void* ptr) {
+  if (!ptr) return;
+  std::lock_guard<std::mutex> lk(g_dense_mu);
+  for (auto& e : g_dense_cache)
+    if (e.ptr == ptr && e.pins > 0) {
+      --e.pins;
+      return;
+    }
+}
+
+// test hook (dctadj_dense_cache_state): entries held / entries pinned now
+static void dense_cache_state(int32_t* entries, int32_t* pinned) {
+  std::lock_guard<std::mutex> lk(g_dense_mu);
+  int np = 0;
+  for (const auto& e : g_dense_cache) np += e.pins > 0;
+  if (entries) *entries = static_cast<int32_t>(g_dense_cache.size());
+  if (pinned) *pinned = np;
 }
 
 struct Launch {
   const KernelEntry* k = nullptr;
   LaunchArgs a;
   std::vector<unsigned char> row_coef, col_coef;
-  void* dense_row = nullptr;
+  void* dense_row = nullptr;  // pinned cache entries (released on reset / destruction)
   void* dense_col = nullptr;
+  Launch() = default;
+  Launch(const Launch&) = delete;
+  Launch& operator=(const Launch&) = delete;
+  ~Launch() { reset(); }
+  void reset() {
+    release_dense(dense_row);
+    release_dense(dense_col);
+    k = nullptr;
+    a = LaunchArgs();
+    row_coef.clear();
+    col_coef.clear();
+    dense_row = dense_col = nullptr;
+  }
 };
 
 static int prepare(Launch& L, const AxisPlan& row, const AxisPlan* col, int dtype, int h, int w,
@@ -438,9 +491,10 @@ static int prepare(Launch& L, const AxisPlan& row, const AxisPlan* col, int dtyp
   return ST_OK;
 }
 
+// the launch is enqueued: unpin its dense matrices (they stay cached)
 static int finish(Launch& L, cudaStream_t st) {
-  (void)st;  // dense matrices stay in the device cache
-  L.dense_row = L.dense_col = nullptr;
+  (void)st;
+  L.reset();
   return ST_OK;
 }
 
@@ -777,7 +831,7 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
         return rc ? rc : rc2;
       }
     }
-    L = Launch();
+    L.reset();
   }
   rc = prepare(L, ph, &pv, dtype, H, W, inverse, in_mode, out_mode, st);
   if (rc == ST_ERR_UNSUPPORTED) {
@@ -785,7 +839,7 @@ static int run_2d(const dctadj_axis* h, const dctadj_axis* v, const void* x, voi
     rc = plan_axis(h, inverse, true, &ph);
     if (!rc) rc = plan_axis(v, inverse, true, &pv);
     if (rc) return rc;
-    L = Launch();
+    L.reset();
     rc = prepare(L, ph, &pv, dtype, H, W, inverse, in_mode, out_mode, st);
     if (rc == ST_ERR_UNSUPPORTED)
       return fail(rc, "no 2-D kernel for %dx%d blocks, dtype %d (mode %d->%d)", H, W, dtype,
@@ -1120,11 +1174,15 @@ static int run_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dc
       return rc;
     }
   }
+  // the error sums are defined on 32x32 tiles (frame_err_kernel): refuse before any work
+  if (err && (h->n != 32 || v->n != 32))
+    return fail(ST_ERR_UNSUPPORTED,
+                "per-frame error sums need 32x32 blocks, got %d x %d (pass err = NULL)", v->n,
+                h->n);
   // unfused: two frame launches + the error reduction
   if ((rc = run_frames(h, v, frames, coefs, nframes, height, width, dtype, false, st))) return rc;
   if ((rc = run_frames(eh, ev, frames, exact, nframes, height, width, dtype, false, st))) return rc;
   if (err) {
-    if (h->n != 32 || v->n != 32) return ST_OK;  // error sums are defined on 32x32 tiles
     const int64_t per_warp = 64, warps = (nblk + per_warp - 1) / per_warp;
     const int grid = static_cast<int>((warps * 32 + 255) / 256);
     const int full = height / 32;
@@ -1304,7 +1362,7 @@ static int run_mixed(const dctadj_mixed* plan, const dctadj_axis* table, const v
     rc = prepare(L, ph, &pv, dtype, v->n, h->n, inverse, MODE_GATHER, MODE_GATHER, cs);
     if (rc == ST_ERR_UNSUPPORTED) {
       if ((rc = plan_axis(h, inverse, true, &ph)) || (rc = plan_axis(v, inverse, true, &pv))) return rc;
-      L = Launch();
+      L.reset();
       rc = prepare(L, ph, &pv, dtype, v->n, h->n, inverse, MODE_GATHER, MODE_GATHER, cs);
       if (rc == ST_ERR_UNSUPPORTED)
         return fail(rc, "no gather kernel for %dx%d blocks, dtype %d", v->n, h->n, dtype);
@@ -1521,6 +1579,7 @@ int dctadj_dense(const double* m, int32_t rows, const void* x, void* y, int64_t 
     dense_rect_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(dm), rows,
                                                      static_cast<const double*>(x),
                                                      static_cast<double*>(y), nvec, n);
+  release_dense(dm);  // the launch is enqueued
   DA_CUDA(cudaGetLastError());
   return ST_OK;
 }
@@ -1741,6 +1800,17 @@ int32_t dctadj_kernel_count(void) {
   int32_t n = 0;
   for (const KernelEntry& e : kRegistry) n += (e.variant == 0);
   return n;
+}
+int dctadj_dense_cache_state(int32_t* entries, int32_t* pinned) {
+  dense_cache_state(entries, pinned);
+  return ST_OK;
+}
+int32_t dctadj_tuning_build(void) {
+#ifdef DCTADJ_TUNING
+  return 1;
+#else
+  return 0;
+#endif
 }
 
 }  // extern "C"

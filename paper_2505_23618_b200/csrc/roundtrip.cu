@@ -77,6 +77,15 @@ constexpr int kG7I = op_code(ST_IDST3, ST_GIVENS, 6);   // band-6 pre DST-7, inv
 constexpr int kG8F = op_code(ST_GIVENS, ST_IDCT2, 6);   // band-6 pre DCT-8 (DCT-3 base)
 constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS, 6);
 
+// TUNE(...) keeps a measured-slower tuning variant in the table only when the
+// library is built with DCTADJ_TUNING=1 (tools/gen_instances.py, Makefile).
+#ifdef DCTADJ_TUNING
+#define TUNE(...) __VA_ARGS__,
+#define TUNEC(...) , __VA_ARGS__
+#else
+#define TUNE(...)
+#define TUNEC(...)
+#endif
 #define RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, NW, VAR)          \
   {DT, H, W, RF, CF, RI, CI, MODE_LINEAR, VAR,                                                   \
    &launch_roundtrip<T, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, NW>}
@@ -89,12 +98,12 @@ constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS, 6);
 // variants 1-4: 4 warps at 255 registers, 3 warps, 2 warps, 4 warps at 128 (941-944);
 // band-6 pre classes: 4 warps at 255 registers with scalar inverse rows (762;
 // packed inverse rows 752, 128 registers 735, 2- / 1-warp CTAs 761-764)
-#define RTG(H, W, RF, CF, RI, CI, PRI, VAR) RTGV(H, W, RF, CF, RI, CI, PRI, 1, 8, VAR), \
-  RTGV(H, W, RF, CF, RI, CI, PRI, 4, 2, VAR + 1), RTGV(H, W, RF, CF, RI, CI, PRI, 3, 3, VAR + 2), \
-  RTGV(H, W, RF, CF, RI, CI, PRI, 2, 4, VAR + 3), RTGV(H, W, RF, CF, RI, CI, PRI, 4, 4, VAR + 4)
-#define RTGP(H, W, RF, CF, RI, CI) RTGV(H, W, RF, CF, RI, CI, false, 4, 2, 0), \
-  RTGV(H, W, RF, CF, RI, CI, true, 4, 4, 1), RTGV(H, W, RF, CF, RI, CI, true, 4, 2, 2), \
-  RTGV(H, W, RF, CF, RI, CI, false, 2, 4, 3), RTGV(H, W, RF, CF, RI, CI, false, 1, 8, 4)
+#define RTG(H, W, RF, CF, RI, CI, PRI, VAR) RTGV(H, W, RF, CF, RI, CI, PRI, 1, 8, VAR)           \
+  TUNEC(RTGV(H, W, RF, CF, RI, CI, PRI, 4, 2, VAR + 1), RTGV(H, W, RF, CF, RI, CI, PRI, 3, 3, VAR + 2), \
+       RTGV(H, W, RF, CF, RI, CI, PRI, 2, 4, VAR + 3), RTGV(H, W, RF, CF, RI, CI, PRI, 4, 4, VAR + 4))
+#define RTGP(H, W, RF, CF, RI, CI) RTGV(H, W, RF, CF, RI, CI, false, 4, 2, 0)                    \
+  TUNEC(RTGV(H, W, RF, CF, RI, CI, true, 4, 4, 1), RTGV(H, W, RF, CF, RI, CI, true, 4, 2, 2),      \
+       RTGV(H, W, RF, CF, RI, CI, false, 2, 4, 3), RTGV(H, W, RF, CF, RI, CI, false, 1, 8, 4))
 #define RT(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, VAR) \
   RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, 1, VAR)
 
@@ -103,40 +112,39 @@ static const RtEntry kRt[] = {
     // 32x32 fp32, sub-block post (config 2): 8 KB super-tiles, 4 warps x (2 + 1) stages,
     // 128-register cap (2 CTAs/SM by shared memory); measured variants in profiles/r01_tuning.md
     RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 4, false, 0),
-    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 2, false, 1),
-    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 3, 3, true, true, false, 2, false, 2),
-    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 3, 2, true, true, false, 3, false, 3),
-    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 4),
-    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 4, false, 5),
-    RT(float, DT_F32, 32, 32, 4, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 6),
+    TUNE(RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 2, false, 1),
+         RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 3, 3, true, true, false, 2, false, 2),
+         RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 3, 2, true, true, false, 3, false, 3),
+         RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 4),
+         RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 4, false, 5),
+         RT(float, DT_F32, 32, 32, 4, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 4, false, 6))
     // (L2 evict-first hints on the loads, the stores or both: no change, 137.9-139.1 us)
     // (16 KB super-tiles shared by two warps, 2 groups x (2 + 1): 156.6-160.2 us)
     // (one-warp CTAs, 8 per SM: 140.6 us sub-8 post, 183.7 us band-6 pre -- no gain here)
     // y stored from registers (no staging tile; measured slower: 0.83 vs 0.90)
-    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 3, true, 7),
-    RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 6, true, 8),
+    TUNE(RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, false, 3, true, 7),
+         RT(float, DT_F32, 32, 32, 2, kSubF, kSubF, kSubI, kSubI, 2, 2, true, true, false, 6, true, 8))
     // 32x32 fp32, band-6 pre (DST-7 / DCT-8 via the DCT-3 base): scalar inverse rows,
     // 255-register budget (177 us per 65,536 blocks; packed inverse rows 188-193 us,
     // y from registers at 12 warps/SM 177 us, 3 warps 219 us)
     RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, false, 2, false, 0),
     RT(float, DT_F32, 32, 32, 2, kG8F, kG8F, kG8I, kG8I, 4, 2, true, true, false, 2, false, 0),
-    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 2, false, 1),
-    RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 3, true, 3),
+    TUNE(RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 2, false, 1),
+         RT(float, DT_F32, 32, 32, 2, kG7F, kG7F, kG7I, kG7I, 4, 2, true, true, true, 3, true, 3))
     // 64x64 fp32 (config 4): built as tuning variants only -- measured slower than
     // the two tile kernels (shared memory holds 4-8 warps/SM at 16 KB per block
     // and 3 buffers per group: sub-8 post 0.52-0.62, band-6 pre 0.44 of the copy
     // peak vs 0.95 / 0.72 for the two kernels), so the default is the two-kernel path
-    RT(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 1, false, 1),
-    RTW(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, false, false, false, 1, false, 2, 2),
-    RTW(float, DT_F32, 64, 64, 1, kG7F, kG7F, kG7I, kG7I, 4, 2, false, false, false, 1, false, 2, 1),
-    // y from registers (no staging tile): 6 two-warp groups x 2 stages = 12 warps/SM
-    RTW(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 6, 2, false, false, false, 1, true, 2, 3),
-    RTW(float, DT_F32, 64, 64, 1, kG7F, kG7F, kG7I, kG7I, 6, 2, false, false, false, 1, true, 2, 3),
-    // (measured, config 4, G coef/s: variant 3 post 824 / pre 530 against 797 / 600 for the two
-    //  kernels; 4 groups x 3 stages 750, one-warp packed groups 697-760)
-    RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 6, 2, false, false, false, 1, true, 2, 3),
-    // (one two-warp group per CTA, 6 CTAs/SM: post 799, pre 572 -- no gain)
-    RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 4, 2, false, false, false, 1, false, 2, 1),
+    // (y from registers, 6 two-warp groups x 2 stages = 12 warps/SM: post 824 / pre 530
+    //  G coef/s against 797 / 600 for the two kernels; 4 groups x 3 stages 750, one-warp
+    //  packed groups 697-760; one two-warp group per CTA, 6 CTAs/SM: post 799, pre 572)
+    TUNE(RT(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, true, true, true, 1, false, 1),
+         RTW(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 4, 2, false, false, false, 1, false, 2, 2),
+         RTW(float, DT_F32, 64, 64, 1, kG7F, kG7F, kG7I, kG7I, 4, 2, false, false, false, 1, false, 2, 1),
+         RTW(float, DT_F32, 64, 64, 1, kSubF, kSubF, kSubI, kSubI, 6, 2, false, false, false, 1, true, 2, 3),
+         RTW(float, DT_F32, 64, 64, 1, kG7F, kG7F, kG7I, kG7I, 6, 2, false, false, false, 1, true, 2, 3),
+         RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 6, 2, false, false, false, 1, true, 2, 3),
+         RTW(float, DT_F32, 64, 64, 1, kG8F, kG8F, kG8I, kG8I, 4, 2, false, false, false, 1, false, 2, 1))
     // config 3 classes: {16,32}^2 shapes, sub-block post (DST-7 / DCT-8 share the ops) and
     // band-6 pre with DST-7 or DCT-8 per axis
     RTG(16, 16, kSubF, kSubF, kSubI, kSubI, false, 0),
@@ -153,6 +161,8 @@ static const RtEntry kRt[] = {
 #undef RTG_PRE
 };
 
+#undef TUNE
+#undef TUNEC
 #undef RT
 #undef RTW
 #undef RTG

@@ -9,10 +9,15 @@ fallback in abi.cu (also listed, per shape).
 """
 from __future__ import annotations
 
+import os
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1] / "paper_2505_23618_b200" / "csrc" / "gen"
-NSHARDS = 24
+NSHARDS_HOT = 12   # gen/inst_hNN.cu: the configs' 2-D kernels, compiled with -lineinfo
+NSHARDS_COLD = 12  # gen/inst_cNN.cu: 1-D primitives, dense composites, copy (no line info)
+# Measured-slower tuning variants (DCTADJ_VARIANT=k) are built only with
+# DCTADJ_TUNING=1; the shipped library holds the defaults alone.
+TUNING = os.environ.get("DCTADJ_TUNING", "0") not in ("", "0")
 
 NONE, DCT2, IDCT2, DST3, IDST3, BAND, SUB, DENSE, GIVENS = range(9)
 
@@ -233,6 +238,8 @@ def instances():
             final.append(inst[:11] + (False, False, 0, pr[2], pr[1]))
         else:
             final.append(inst[:11] + (pr and cc != ID, pc, 0, 0))
+        if not TUNING:
+            continue
         if (im, om) == (2, 2):
             binv = cf and (rc >> 8) in (4, 6) and (rc & 15) != SUB and ((rc >> 4) & 15) in (BAND, GIVENS)
             exps = GATHER_BINV_EXPERIMENT if binv else GATHER_EXPERIMENT
@@ -272,25 +279,58 @@ def _write_if_changed(path: Path, text: str) -> None:
         path.write_text(text)
 
 
+def is_hot(inst) -> bool:
+    """The BASELINE configs' 2-D kernels -- built with -lineinfo so ncu's source
+    page maps onto them: every gather (C3) and frame (C5) kernel, and the linear
+    fp32 32x32 / 64x64 and fp64 32x32 kernels of the sub-8 post and same-kind
+    band-6 (Givens) pre pairs (C1, C2, C4)."""
+    dt, h, w, p, rc, cc, cf, im, om = inst[:9]
+    if cc == ID or rc == code(DENSE):
+        return False  # 1-D primitives, copy tiles, dense composites
+    if (im, om) != (0, 0):
+        return True
+    if (dt, h, w) not in (("float", 32, 32), ("float", 64, 64), ("double", 32, 32)):
+        return False
+    sub = {code(DCT2, SUB, 8), code(SUB, IDCT2, 8)}
+    g6 = {code(GIVENS, DST3, 6), code(IDST3, GIVENS, 6), code(GIVENS, IDCT2, 6),
+          code(DCT2, GIVENS, 6)}
+    return rc == cc and (rc in sub or rc in g6)
+
+
 def main():
     ROOT.mkdir(parents=True, exist_ok=True)
     insts = instances()
-    shards = [[] for _ in range(NSHARDS)]
+    hot = [[] for _ in range(NSHARDS_HOT)]
+    cold = [[] for _ in range(NSHARDS_COLD)]
     seen = set()
-    for i, inst in enumerate(insts):
+    nh = nc = 0
+    for inst in insts:
         if _targs(inst) in seen:  # a tuning variant equal to a default: one definition
             continue
         seen.add(_targs(inst))
-        shards[i % NSHARDS].append(inst)
+        if is_hot(inst):
+            hot[nh % NSHARDS_HOT].append(inst)
+            nh += 1
+        else:
+            cold[nc % NSHARDS_COLD].append(inst)
+            nc += 1
     reg = ["// Generated by tools/gen_instances.py -- do not edit.",
-           f"// {len(insts)} tile_kernel instantiations."]
-    for k, shard in enumerate(shards):
-        lines = ["// Generated by tools/gen_instances.py -- do not edit.",
-                 '#include "../launch.cuh"', "", "namespace dctadj {", ""]
-        for inst in shard:
-            lines.append(f"template int launch_tile<{_targs(inst)}>(const LaunchArgs&);")
-        lines += ["", "}  // namespace dctadj", ""]
-        _write_if_changed(ROOT / f"inst_{k:02d}.cu", "\n".join(lines))
+           f"// {len(insts)} tile_kernel instantiations ({nh} hot, {nc} cold)"
+           f"{' + tuning variants' if TUNING else ''}."]
+    wanted = set()
+    for tag, shards in (("h", hot), ("c", cold)):
+        for k, shard in enumerate(shards):
+            lines = ["// Generated by tools/gen_instances.py -- do not edit.",
+                     '#include "../launch.cuh"', "", "namespace dctadj {", ""]
+            for inst in shard:
+                lines.append(f"template int launch_tile<{_targs(inst)}>(const LaunchArgs&);")
+            lines += ["", "}  // namespace dctadj", ""]
+            name = f"inst_{tag}{k:02d}.cu"
+            wanted.add(name)
+            _write_if_changed(ROOT / name, "\n".join(lines))
+    for stale in ROOT.glob("inst_*.cu"):
+        if stale.name not in wanted:
+            stale.unlink()
     decl = []
     rows = []
     declared = set()
@@ -304,7 +344,8 @@ def main():
                     f"&launch_tile<{targs}>}},")
     reg += decl + ["", "static const KernelEntry kRegistry[] = {"] + rows + ["};", ""]
     _write_if_changed(ROOT / "registry.inc", "\n".join(reg))
-    print(f"{len(insts)} instantiations in {NSHARDS} shards")
+    print(f"{len(insts)} instantiations: {nh} hot + {nc} cold in "
+          f"{NSHARDS_HOT} + {NSHARDS_COLD} shards")
 
 
 if __name__ == "__main__":
