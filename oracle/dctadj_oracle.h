@@ -32,6 +32,22 @@ int or_adjusted_2d_f32(const or_axis* ah, const or_axis* av, int inverse,
                        const float* x, float* y, int64_t nblk, int threads);
 int or_num_threads_available(void);
 
+/* full-batch parity checkers (see dctadj_oracle.c); dtype 0 = fp32, 1 = fp64 */
+typedef struct {
+  double max_err; /* worst per-block normwise relative error */
+  int64_t worst;  /* its block index (-1: no blocks) */
+  int64_t over;   /* blocks with error > tol */
+} or_check_result;
+int or_check_2d(const or_axis* ah, const or_axis* av, int inverse, int dtype, const void* x,
+                const void* y, int64_t nblk, int threads, double tol, or_check_result* res);
+int or_check_mixed(const or_axis* table, int ntable, const int32_t* h_index,
+                   const int32_t* v_index, const int64_t* offsets, int64_t nblk, int inverse,
+                   int dtype, const void* x, const void* y, int threads, double tol,
+                   or_check_result* res);
+int or_check_frames(const or_axis* ah, const or_axis* av, int inverse, const float* frames,
+                    const float* coefs, int nframes, int height, int width, int threads,
+                    double tol, or_check_result* res);
+
 #ifdef __cplusplus
 }
 #endif

@@ -224,3 +224,104 @@ class RefPipeline:
         cols = np.ascontiguousarray(np.asarray(y, dtype=float).transpose(0, 2, 1)).reshape(b * w, h)
         t = np.ascontiguousarray(self.inverse(av, cols).reshape(b, w, h).transpose(0, 2, 1))
         return self.inverse(ah, t.reshape(b * h, w)).reshape(b, h, w)
+
+
+# ------------------------------------------------------------------ full-batch checkers
+class _CheckResult(ctypes.Structure):
+    _fields_ = [("max_err", ctypes.c_double), ("worst", ctypes.c_int64), ("over", ctypes.c_int64)]
+
+
+def _check_lib():
+    lb = lib()
+    if not getattr(lb, "_check_typed", False):
+        ap, vp = ctypes.POINTER(_Axis), ctypes.c_void_p
+        i32p, i64p = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)
+        rp = ctypes.POINTER(_CheckResult)
+        lb.or_check_2d.argtypes = [ap, ap, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int64,
+                                   ctypes.c_int, ctypes.c_double, rp]
+        lb.or_check_mixed.argtypes = [ap, ctypes.c_int, i32p, i32p, i64p, ctypes.c_int64,
+                                      ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int,
+                                      ctypes.c_double, rp]
+        lb.or_check_frames.argtypes = [ap, ap, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_double, rp]
+        lb._check_typed = True
+    return lb
+
+
+def _dtype_code(a: np.ndarray) -> int:
+    if a.dtype == np.float32:
+        return 0
+    if a.dtype == np.float64:
+        return 1
+    raise TypeError(f"checker needs float32 / float64 arrays, got {a.dtype}")
+
+
+def _result(r: _CheckResult, nblk: int) -> dict:
+    return {"max_err": float(r.max_err), "worst_block": int(r.worst), "over_tol": int(r.over),
+            "blocks": int(nblk)}
+
+
+def check_2d(ah: OAxis, av: OAxis, x, y, inverse=False, threads=None, tol=0.0) -> dict:
+    """Every block of y against the oracle applied to x ((nblk, H, W), same dtype):
+    {max_err, worst_block, over_tol, blocks} (per-block normwise relative error)."""
+    x, y = np.ascontiguousarray(x), np.ascontiguousarray(y)
+    if x.shape != y.shape or x.dtype != y.dtype or x.ndim != 3:
+        raise ValueError(f"check_2d: x {x.shape} {x.dtype} vs y {y.shape} {y.dtype}")
+    ch, _kh = ah.c()
+    cv, _kv = av.c()
+    r = _CheckResult()
+    rc = _check_lib().or_check_2d(ctypes.byref(ch), ctypes.byref(cv), int(inverse), _dtype_code(x),
+                                  x.ctypes.data, y.ctypes.data, x.shape[0],
+                                  threads or threads_available(), float(tol), ctypes.byref(r))
+    if rc:
+        raise ValueError("or_check_2d: bad geometry")
+    return _result(r, x.shape[0])
+
+
+def check_mixed(table, h_index, v_index, offsets, x, y, inverse=False, threads=None,
+                tol=0.0) -> dict:
+    """Packed mixed-shape batch (config 3): block i at offsets[i], rows through
+    table[h_index[i]], columns through table[v_index[i]]."""
+    x, y = np.ascontiguousarray(x), np.ascontiguousarray(y)
+    if x.shape != y.shape or x.dtype != y.dtype:
+        raise ValueError("check_mixed: x / y mismatch")
+    axes = (_Axis * len(table))()
+    keep = []
+    for k, ax in enumerate(table):
+        c, m = ax.c()
+        axes[k] = c
+        keep.append(m)
+    hi = np.ascontiguousarray(h_index, dtype=np.int32)
+    vi = np.ascontiguousarray(v_index, dtype=np.int32)
+    of = np.ascontiguousarray(offsets, dtype=np.int64)
+    r = _CheckResult()
+    rc = _check_lib().or_check_mixed(
+        axes, len(table), hi.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+        vi.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+        of.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(of), int(inverse), _dtype_code(x),
+        x.ctypes.data, y.ctypes.data, threads or threads_available(), float(tol), ctypes.byref(r))
+    if rc:
+        raise ValueError("or_check_mixed: bad table index or size")
+    return _result(r, len(of))
+
+
+def check_frames(ah: OAxis, av: OAxis, frames, coefs, inverse=False, threads=None,
+                 tol=0.0) -> dict:
+    """fp32 frame stack (F, height, width) vs block-major coefficients (config 5;
+    bottom zero padding, SURVEY.md App. A D6).  Forward: coefs vs oracle(frames);
+    inverse: frames vs oracle^-1(coefs), rows inside the frame only."""
+    frames = np.ascontiguousarray(frames, dtype=np.float32)
+    coefs = np.ascontiguousarray(coefs, dtype=np.float32)
+    f, height, width = frames.shape
+    ch, _kh = ah.c()
+    cv, _kv = av.c()
+    ty, tx = -(-height // av.n), width // ah.n
+    if coefs.size != f * ty * tx * ah.n * av.n:
+        raise ValueError(f"check_frames: {coefs.shape} coefficients for {frames.shape} frames")
+    r = _CheckResult()
+    rc = _check_lib().or_check_frames(ctypes.byref(ch), ctypes.byref(cv), int(inverse),
+                                      frames.ctypes.data, coefs.ctypes.data, f, height, width,
+                                      threads or threads_available(), float(tol), ctypes.byref(r))
+    if rc:
+        raise ValueError("or_check_frames: bad geometry")
+    return _result(r, f * ty * tx)

@@ -131,3 +131,55 @@ def test_against_reference_core_if_built():
     xb = rng.standard_normal((3, 32, 32))
     assert np.array_equal(O.adjusted_2d(adj, adj, xb), ref.forward_2d(adj, adj, xb))
     assert np.array_equal(O.adjusted_2d(adj, adj, xb, inverse=True), ref.inverse_2d(adj, adj, xb))
+
+
+# ------------------------------------------------------------------ full-batch checkers
+def test_check_2d_against_golden(golden):
+    """The checkers the full-size GPU gates use: zero error on the reference's own
+    outputs, and a perturbed / NaN block is found and counted."""
+    a6 = oaxis(matio.load_designed("band6_pre_dst3_dst7_n32"))
+    r = O.check_2d(a6, a6, golden["c1/x"], golden["c1/y"], tol=1e-9)
+    assert r["max_err"] == 0.0 and r["over_tol"] == 0 and r["blocks"] == 6
+    s8 = oaxis(dct8_adjustment_from_dst7(matio.load_designed("sub8_post_dct2_dst7_n32")))
+    x32 = golden["c2/x"]
+    y32 = golden["c2/y"].astype(np.float32)
+    r = O.check_2d(s8, s8, x32, y32, tol=1e-5)
+    assert r["max_err"] < 1e-7 and r["over_tol"] == 0  # fp32 rounding of the golden output only
+    r = O.check_2d(s8, s8, y32, golden["c2/xr"].astype(np.float32), inverse=True, tol=1e-5)
+    assert r["max_err"] < 1e-6
+    bad = y32.copy()
+    bad[4, 7, 7] += 0.01 * np.abs(bad[4]).max()
+    bad[1, 0, 3] = np.nan
+    r = O.check_2d(s8, s8, x32, bad, tol=1e-5, threads=3)
+    assert r["over_tol"] == 2 and r["worst_block"] == 1 and r["max_err"] == np.inf
+
+
+def test_check_mixed_and_frames_against_golden(golden):
+    pre = {n: matio.load_designed(f"band6_pre_dst3_dst7_n{n}") for n in (16, 32)}
+    table = [oaxis(pre[16]), oaxis(flip_pre_adjustment(pre[16])), oaxis(pre[32]),
+             oaxis(flip_pre_adjustment(pre[32]))]
+    xs, ys, hi, vi, offs = [], [], [], [], []
+    off = 0
+    for h, w in ((16, 16), (16, 32), (32, 16), (32, 32)):
+        x = golden[f"c3/{h}x{w}/x"].astype(np.float64)
+        for kh, kv in (("dst7", "dct8"), ("dct8", "dst7")):
+            y = golden[f"c3/{h}x{w}/pre/{kh}_{kv}/y"]
+            for b in range(x.shape[0]):
+                xs.append(x[b].ravel())
+                ys.append(y[b].ravel())
+                hi.append((0 if w == 16 else 2) + (kh == "dct8"))
+                vi.append((0 if h == 16 else 2) + (kv == "dct8"))
+                offs.append(off)
+                off += h * w
+    xp, yp = np.concatenate(xs), np.concatenate(ys)
+    r = O.check_mixed(table, hi, vi, offs, xp, yp, tol=1e-9)
+    assert r["max_err"] < 1e-13 and r["over_tol"] == 0 and r["blocks"] == len(offs)
+    yp[offs[5] + 3] += 1.0
+    assert O.check_mixed(table, hi, vi, offs, xp, yp, tol=1e-9)["worst_block"] == 5
+    # frames (config 5): padded 48 -> 64 rows, block-major coefficients
+    s7 = oaxis(matio.load_designed("sub8_post_dct2_dst7_n32"))
+    fr = golden["c5/frames"]
+    r = O.check_frames(s7, s7, fr, golden["c5/y"].astype(np.float32), tol=1e-5)
+    assert r["max_err"] < 1e-6 and r["blocks"] == golden["c5/y"].shape[0]
+    inv = O.check_frames(s7, s7, fr, golden["c5/y"].astype(np.float32), inverse=True, tol=1e-5)
+    assert inv["max_err"] < 1e-5
