@@ -44,22 +44,30 @@ def weighted_ranges(weights, world: int) -> list[tuple[int, int]]:
 
 @dataclass
 class Stats:
-    elapsed_ms: float = 0.0       # max over ranks
+    elapsed_ms: float = 0.0       # max over ranks (device-timed region)
     coefficients: int = 0         # sum
     err_energy: float = 0.0       # sum  ||Y_adj - Y_exact||^2
     ref_energy: float = 0.0       # sum  ||Y_exact||^2
     max_rel_err: float = 0.0      # max
+    e2e_ms: float = 0.0           # max (host-buffer step)
+    err_energy_full: float = 0.0  # sum, unpadded tile rows only (config 5)
+    ref_energy_full: float = 0.0  # sum, unpadded tile rows only
 
 
 def reduce_stats(stats: Stats, device=None) -> Stats:
-    """All-reduce the per-rank scalars (no-op without an initialised group)."""
+    """All-reduce the per-rank scalars (no-op without an initialised group):
+    MAX of the times and the error, SUM of the counts and energies."""
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return stats
-    mx = torch.tensor([stats.elapsed_ms, stats.max_rel_err], dtype=torch.float64, device=device)
-    sm = torch.tensor([float(stats.coefficients), stats.err_energy, stats.ref_energy],
-                      dtype=torch.float64, device=device)
+    mx = torch.tensor([stats.elapsed_ms, stats.max_rel_err, stats.e2e_ms], dtype=torch.float64,
+                      device=device)
+    sm = torch.tensor([float(stats.coefficients), stats.err_energy, stats.ref_energy,
+                       stats.err_energy_full, stats.ref_energy_full], dtype=torch.float64,
+                      device=device)
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-    return Stats(float(mx[0]), int(round(float(sm[0]))), float(sm[1]), float(sm[2]), float(mx[1]))
+    return Stats(elapsed_ms=float(mx[0]), coefficients=int(round(float(sm[0]))),
+                 err_energy=float(sm[1]), ref_energy=float(sm[2]), max_rel_err=float(mx[1]),
+                 e2e_ms=float(mx[2]), err_energy_full=float(sm[3]), ref_energy_full=float(sm[4]))

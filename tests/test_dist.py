@@ -60,3 +60,50 @@ def test_two_rank_sharded_roundtrip():
     assert all(r[5] == 2.0 for r in res)       # MAX of elapsed
     assert all(r[6] < 1e-12 for r in res)
     assert res[0][7] == res[1][7]
+
+
+def _dry_run(gpus: int, scaling: str = "strong") -> dict:
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", str(gpus), "--dry-run",
+                        "--scaling", scaling], capture_output=True, text=True, timeout=240,
+                       env=env, cwd=root)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("gpus", [2, 3])
+def test_bench_spawns_ranks_that_cover_each_config_once(gpus):
+    """`bench.py --gpus N` self-launches N ranks (torchrun; gloo in --dry-run):
+    their shards tile every BASELINE config exactly once (C1/C2/C4 block ranges,
+    C3 equal-coefficient ranges, C5 frames), and the post-timing reduction sums
+    the per-rank coefficient counts and takes the max of the times."""
+    out = _dry_run(gpus)
+    assert out["world"] == gpus
+    full = _dry_run(1)
+    for cfg, per_rank in out["per_rank"].items():
+        assert len(per_rank) == gpus
+        assert per_rank[0][0] == 0 and per_rank[-1][1] == out["totals"][cfg]
+        for a, b in zip(per_rank, per_rank[1:]):
+            assert a[1] == b[0] and a[0] <= a[1]  # contiguous, no gap, no overlap
+        assert out["coefficients"][cfg] == full["coefficients"][cfg]  # same total work
+    c3 = [b - a for a, b in out["per_rank"]["c3_pre"]]
+    assert max(c3) - min(c3) < 0.01 * sum(c3)  # equal coefficient counts, not block counts
+    assert out["reduced"]["c2_coefficients_sum"] == 65536 * 1024
+    assert out["reduced"]["elapsed_ms_max"] == float(gpus)
+    assert full["coefficients"]["c4_dst7_pre"] == 262144 * 4096
+    assert full["coefficients"]["c5"] == 64 * 68 * 120 * 1024
+
+
+@pytest.mark.timeout(300)
+def test_bench_weak_scaling_gives_every_rank_the_config():
+    out = _dry_run(2, "weak")
+    for cfg, per_rank in out["per_rank"].items():
+        assert per_rank == [[0, out["totals"][cfg]]] * 2
