@@ -204,7 +204,7 @@ class ClockSampler:
                         pass
                     time.sleep(0.0005)
                 else:
-                    time.sleep(0.002)
+                    time.sleep(0.0002)
             return
         try:  # fallback: one long-running nvidia-smi
             proc = subprocess.Popen(
@@ -237,13 +237,33 @@ class ClockSampler:
             p.terminate()
         self._t.join(timeout=5)
 
+    def _sample_now(self):
+        """One synchronous NVML sample (region boundaries: a region of a few ms can
+        end before the polling thread is scheduled)."""
+        if self._nv is None:
+            return
+        nv = self._nv
+        try:
+            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.samples.append((self.region, float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)),
+                                 int(get_r(self._h))))
+        except Exception:
+            pass
+
     def mark_start(self):
+        """Called with the previous work drained, right before the first event of
+        the region is recorded: samples the clocks as the region opens."""
         self.region += 1
+        self._sample_now()
         self.active = True
 
+    def sample_in_region(self):
+        """A sample taken while the region's kernels are still queued / running."""
+        self._sample_now()
+
     def mark_end(self):
-        if self.source == "nvml":  # one sample right at the end of a short region
-            time.sleep(0.001)
+        self._sample_now()
         self.active = False
 
     def summary(self, all_regions: bool = False) -> dict:
@@ -848,6 +868,7 @@ def measure(w: Workload, args, rank: int, world: int, clk: ClockSampler, threads
     for i in range(args.steps):
         w.step(i)
     e1.record(stream)
+    clk.sample_in_region()  # the launches are queued: the GPU is running them now
     torch.cuda.synchronize()
     clk.mark_end()
     if world > 1:
