@@ -18,6 +18,7 @@
 #include "dense_tc.cuh"
 #include "dense_tc64.cuh"
 #include "enc5.cuh"
+#include "frames_exact.cuh"
 #include "launch.cuh"
 #include "roundtrip.cuh"
 
@@ -712,6 +713,59 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
 }
 
 // 64x64 fp32 dense on the tensor cores (dense_tc64.cuh), LINEAR blocks
+// config 5's fused step with role-specific register budgets (frames_exact.cuh)
+template <int FRC, int FCC>
+static int launch_frames_exact(const LaunchArgs& a, int64_t nblocks, int tiles_y, int tiles_x,
+                               const FusedArgs& fz) {
+  constexpr int S = 5;  // 5 x 16 KB ring + 3 exact + 4 adjusted 16 KB tiles: 208 KB, one CTA/SM
+  Geom g{};
+  g.nblocks = nblocks;
+  g.ntiles = (nblocks + 3) / 4;
+  g.tiles_y = tiles_y;
+  g.tiles_x = tiles_x;
+  if (g.ntiles == 0) return ST_OK;
+  LaunchArgs la = a;
+  la.rows = nblocks * 32;
+  CUtensorMap in_map, out_map, adj_map;
+  {  // frames: {col in block, block column, frame row, frame}, one box = 4 blocks
+    uint64_t dims[4] = {32, static_cast<uint64_t>(tiles_x), static_cast<uint64_t>(a.frame_h),
+                        static_cast<uint64_t>(a.frames)};
+    uint64_t strides[3] = {128, static_cast<uint64_t>(a.frame_w) * 4,
+                           static_cast<uint64_t>(a.frame_w) * a.frame_h * 4};
+    uint32_t box[4] = {32, 4, 32, 1};
+    int rc = encode_tensor_map(&in_map, DT_F32, 4, dims, strides, box, 128, const_cast<void*>(a.in));
+    if (rc) return rc;
+  }
+  int rc = make_map<float, 32, 32, 4, MODE_LINEAR>(&out_map, a.out, la);
+  if (!rc) rc = make_map<float, 32, 32, 4, MODE_LINEAR_IL>(&adj_map, fz.adj_out, la);
+  if (rc) return rc;
+  KParams<float, 32, 32, FRC, FCC> kp;
+  std::memset(&kp, 0, sizeof(kp));
+  using RowOp = AxisOp<float, 32, FRC>;
+  using ColOp = AxisOp<float, 32, FCC>;
+  if (RowOp::NCOEF > 0) std::memcpy(kp.row.c, fz.row_coef, sizeof(float) * RowOp::NCOEF);
+  if (ColOp::NCOEF > 0) std::memcpy(kp.col.c, fz.col_coef, sizeof(float) * ColOp::NCOEF);
+  DenseTcParams prm{static_cast<const float*>(a.dense_row), static_cast<const float*>(a.dense_col),
+                    nullptr, nullptr, fz.err, a.frame_h, 0};
+  if ((rc = stream_sched_counter(a.stream, &prm.sched))) return rc;
+  auto kern = frames_exact_kernel<S, FRC, FCC>;
+  constexpr size_t smem = frames_exact_smem<S>();
+  static std::atomic<int> setup[kMaxDevices];
+  if (!kernel_blocks_per_sm(kern, kFxThreads, smem, setup, "frames_exact_kernel")) return ST_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(g.ntiles, num_sms_cached())));
+  cfg.blockDim = dim3(kFxThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm, adj_map, kp));
+  return ST_OK;
+}
+
 static int launch_dense_tc64(const LaunchArgs& a, int64_t nblocks) {
   constexpr int S = 3;  // 3 x 32 KB ring + 2 x 32 KB staging + 64 KB matrices: 224 KB
   constexpr int NG = kTc64Groups;
@@ -1167,9 +1221,18 @@ static int run_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dc
       a.dense_col = L.dense_col;
       a.stream = st;
       FusedArgs fz{coefs, rcf.data(), ccf.data(), err};
-      rc = ph.code == kSub8
-               ? launch_dense_tc<MODE_FRAME4, MODE_LINEAR, kSub8, kSub8>(a, nblk, ty, tx, &fz)
-               : launch_dense_tc<MODE_FRAME4, MODE_LINEAR, kGiv6, kGiv6>(a, nblk, ty, tx, &fz);
+      // DCTADJ_FX_LEGACY=1: the single-role fused kernel (dense_tc.cuh FUSED), for comparison
+      static const bool legacy = [] {
+        const char* e = std::getenv("DCTADJ_FX_LEGACY");
+        return e && e[0] == '1';
+      }();
+      if (legacy)
+        rc = ph.code == kSub8
+                 ? launch_dense_tc<MODE_FRAME4, MODE_LINEAR, kSub8, kSub8>(a, nblk, ty, tx, &fz)
+                 : launch_dense_tc<MODE_FRAME4, MODE_LINEAR, kGiv6, kGiv6>(a, nblk, ty, tx, &fz);
+      else
+        rc = ph.code == kSub8 ? launch_frames_exact<kSub8, kSub8>(a, nblk, ty, tx, fz)
+                              : launch_frames_exact<kGiv6, kGiv6>(a, nblk, ty, tx, fz);
       if (trace_on()) std::fprintf(stderr, "[dctadj] frames_exact: fused (rc %d)\n", rc);
       return rc;
     }

@@ -322,9 +322,12 @@ DA_DEV void scale_out(V (&v)[N]) {
 // Row pass: lane owns a row (PAIR: two rows, rho and rho + GT, packed as f2
 // lanes).  Rows are read/written as 16-byte chunks: conflict-free under the
 // swizzle (8 lanes of a phase hit 8 distinct chunk columns).
+//
+// row_pass_io reads the tile from `in` and writes the result to `out` (same
+// layout; in == out is the in-place pass).
 template <typename T, int H, int W, int P, int RC, int GSQ, bool PAIR, int GT = 32>
-DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Coef& cf,
-                     const T* dense) {
+DA_DEV void row_pass_io(const uint8_t* in, uint8_t* out, int lane,
+                        const typename AxisOp<T, W, RC>::Coef& cf, const T* dense) {
   using L = TileLayout<T, H, W, P>;
   constexpr int PER16 = 16 / sizeof(T);
   constexpr int ROWS_PER_IT = PAIR ? 2 * GT : GT;
@@ -336,7 +339,7 @@ DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Co
       T v[W];
 #pragma unroll
       for (int q = 0; q < W / PER16; ++q) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(buf + L::addr(rho, q * 16));
+        const uint4 raw = *reinterpret_cast<const uint4*>(in + L::addr(rho, q * 16));
         const T* e = reinterpret_cast<const T*>(&raw);
 #pragma unroll
         for (int k = 0; k < PER16; ++k) v[q * PER16 + k] = e[k];
@@ -349,15 +352,15 @@ DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Co
         T* e = reinterpret_cast<T*>(&raw);
 #pragma unroll
         for (int k = 0; k < PER16; ++k) e[k] = v[q * PER16 + k];
-        *reinterpret_cast<uint4*>(buf + L::addr(rho, q * 16)) = raw;
+        *reinterpret_cast<uint4*>(out + L::addr(rho, q * 16)) = raw;
       }
     } else {
       static_assert(sizeof(T) == 4, "packed rows are fp32 pairs");
       f2 v[W];
 #pragma unroll
       for (int q = 0; q < W / 4; ++q) {
-        const float4 a = *reinterpret_cast<const float4*>(buf + L::addr(rho, q * 16));
-        const float4 b = *reinterpret_cast<const float4*>(buf + L::addr(rho + GT, q * 16));
+        const float4 a = *reinterpret_cast<const float4*>(in + L::addr(rho, q * 16));
+        const float4 b = *reinterpret_cast<const float4*>(in + L::addr(rho + GT, q * 16));
         v[4 * q + 0].v = make_float2(a.x, b.x);
         v[4 * q + 1].v = make_float2(a.y, b.y);
         v[4 * q + 2].v = make_float2(a.z, b.z);
@@ -367,13 +370,19 @@ DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Co
       scale_out<f2, W, GSQ>(v);
 #pragma unroll
       for (int q = 0; q < W / 4; ++q) {
-        *reinterpret_cast<float4*>(buf + L::addr(rho, q * 16)) =
+        *reinterpret_cast<float4*>(out + L::addr(rho, q * 16)) =
             make_float4(v[4 * q].v.x, v[4 * q + 1].v.x, v[4 * q + 2].v.x, v[4 * q + 3].v.x);
-        *reinterpret_cast<float4*>(buf + L::addr(rho + GT, q * 16)) =
+        *reinterpret_cast<float4*>(out + L::addr(rho + GT, q * 16)) =
             make_float4(v[4 * q].v.y, v[4 * q + 1].v.y, v[4 * q + 2].v.y, v[4 * q + 3].v.y);
       }
     }
   }
+}
+
+template <typename T, int H, int W, int P, int RC, int GSQ, bool PAIR, int GT = 32>
+DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Coef& cf,
+                     const T* dense) {
+  row_pass_io<T, H, W, P, RC, GSQ, PAIR, GT>(buf, buf, lane, cf, dense);
 }
 
 // Column pass: lane owns a column (PAIR: two adjacent columns read as one
