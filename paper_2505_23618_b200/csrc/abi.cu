@@ -18,7 +18,9 @@
 #include "dense_tc.cuh"
 #include "dense_tc64.cuh"
 #include "enc5.cuh"
+#ifdef DCTADJ_TUNING
 #include "frames_exact.cuh"
+#endif
 #include "launch.cuh"
 #include "roundtrip.cuh"
 
@@ -712,12 +714,12 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   return ST_OK;
 }
 
-// 64x64 fp32 dense on the tensor cores (dense_tc64.cuh), LINEAR blocks
+#ifdef DCTADJ_TUNING
 // config 5's fused step with role-specific register budgets (frames_exact.cuh)
 template <int FRC, int FCC>
 static int launch_frames_exact(const LaunchArgs& a, int64_t nblocks, int tiles_y, int tiles_x,
                                const FusedArgs& fz) {
-  constexpr int S = 5;  // 5 x 16 KB ring + 3 exact + 4 adjusted 16 KB tiles: 208 KB, one CTA/SM
+  constexpr int S = 5;  // 5 x 16 KB ring + 2 x 2 exact 16 KB tiles + 8 adjusted 8 KB half-tiles: 224 KB
   Geom g{};
   g.nblocks = nblocks;
   g.ntiles = (nblocks + 3) / 4;
@@ -737,7 +739,7 @@ static int launch_frames_exact(const LaunchArgs& a, int64_t nblocks, int tiles_y
     if (rc) return rc;
   }
   int rc = make_map<float, 32, 32, 4, MODE_LINEAR>(&out_map, a.out, la);
-  if (!rc) rc = make_map<float, 32, 32, 4, MODE_LINEAR_IL>(&adj_map, fz.adj_out, la);
+  if (!rc) rc = make_map<float, 32, 32, 2, MODE_LINEAR>(&adj_map, fz.adj_out, la);  // half-tiles
   if (rc) return rc;
   KParams<float, 32, 32, FRC, FCC> kp;
   std::memset(&kp, 0, sizeof(kp));
@@ -765,7 +767,9 @@ static int launch_frames_exact(const LaunchArgs& a, int64_t nblocks, int tiles_y
   DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm, adj_map, kp));
   return ST_OK;
 }
+#endif  // DCTADJ_TUNING
 
+// 64x64 fp32 dense on the tensor cores (dense_tc64.cuh), LINEAR blocks
 static int launch_dense_tc64(const LaunchArgs& a, int64_t nblocks) {
   constexpr int S = 3;  // 3 x 32 KB ring + 2 x 32 KB staging + 64 KB matrices: 224 KB
   constexpr int NG = kTc64Groups;
@@ -1221,18 +1225,21 @@ static int run_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dc
       a.dense_col = L.dense_col;
       a.stream = st;
       FusedArgs fz{coefs, rcf.data(), ccf.data(), err};
-      // DCTADJ_FX_LEGACY=1: the single-role fused kernel (dense_tc.cuh FUSED), for comparison
-      static const bool legacy = [] {
-        const char* e = std::getenv("DCTADJ_FX_LEGACY");
+      // the single-role fused kernel (dense_tc.cuh FUSED); the warp-specialised
+      // variant (frames_exact.cuh, measured slower) only in DCTADJ_TUNING builds
+#ifdef DCTADJ_TUNING
+      static const bool ws = [] {
+        const char* e = std::getenv("DCTADJ_FX_WS");
         return e && e[0] == '1';
       }();
-      if (legacy)
+      if (ws)
+        rc = ph.code == kSub8 ? launch_frames_exact<kSub8, kSub8>(a, nblk, ty, tx, fz)
+                              : launch_frames_exact<kGiv6, kGiv6>(a, nblk, ty, tx, fz);
+      else
+#endif
         rc = ph.code == kSub8
                  ? launch_dense_tc<MODE_FRAME4, MODE_LINEAR, kSub8, kSub8>(a, nblk, ty, tx, &fz)
                  : launch_dense_tc<MODE_FRAME4, MODE_LINEAR, kGiv6, kGiv6>(a, nblk, ty, tx, &fz);
-      else
-        rc = ph.code == kSub8 ? launch_frames_exact<kSub8, kSub8>(a, nblk, ty, tx, fz)
-                              : launch_frames_exact<kGiv6, kGiv6>(a, nblk, ty, tx, fz);
       if (trace_on()) std::fprintf(stderr, "[dctadj] frames_exact: fused (rc %d)\n", rc);
       return rc;
     }
