@@ -163,6 +163,32 @@ int launch_tile(const LaunchArgs& a) {
   if (RowOp::NCOEF > 0) std::memcpy(prm.row.c, a.row_coef, sizeof(T) * RowOp::NCOEF);
   if (ColOp::NCOEF > 0) std::memcpy(prm.col.c, a.col_coef, sizeof(T) * ColOp::NCOEF);
 
+  if constexpr ((CH & 8) != 0) {  // shared-ring kernel: NG compute warps + a producer, S stages
+    static_assert(P == 1 && IN_MODE == MODE_LINEAR && OUT_MODE == MODE_LINEAR,
+                  "the ring kernel moves whole LINEAR blocks");
+    auto kern = ring_kernel<T, H, W, RC, CC, COL_FIRST, NG, S>;
+    const size_t smem = 1024 + static_cast<size_t>(S) * L::STAGEB + 2 * S * 8;
+    static std::atomic<int> setup[kMaxDevices];
+    if (!kernel_blocks_per_sm(kern, (NG + 1) * 32, smem, setup, "ring_kernel")) return ST_ERR_CUDA;
+    const int64_t cap = num_sms_cached();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(g.ntiles < cap ? g.ntiles : cap));
+    cfg.blockDim = dim3((NG + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = a.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_last_error("ring_kernel launch: %s", cudaGetErrorString(e));
+      return ST_ERR_CUDA;
+    }
+    return ST_OK;
+  } else {
   auto kern = tile_kernel<T, H, W, P, RC, CC, COL_FIRST, IN_MODE, OUT_MODE, NG, S, PAIR_ROW, PAIR_COL, CH, NW>;
   const size_t dense_bytes =
       sizeof(T) * ((RowOp::kDense ? W * W : 0) + (ColOp::kDense ? H * H : 0));
@@ -192,6 +218,7 @@ int launch_tile(const LaunchArgs& a) {
     return ST_ERR_CUDA;
   }
   return ST_OK;
+  }
 }
 
 }  // namespace dctadj

@@ -439,7 +439,8 @@ DA_DEV void group_sync(int grp) {
 template <typename T, int H, int W, int P, int RC, int CC, bool COL_FIRST, int IN_MODE,
           int OUT_MODE, int NG, int S, bool PAIR_ROW = false, bool PAIR_COL = false, int CH = 0,
           int NW = 1>
-// CH bits 0-1: L2 hints; bits 4+: minimum resident CTAs per SM (register cap)
+// CH bits 0-1: L2 hints; bit 3: the launcher runs ring_kernel instead (below);
+// bits 4+: minimum resident CTAs per SM (register cap)
 __global__ void __launch_bounds__(NG * NW * 32, (CH >> 4) > 0 ? (CH >> 4) : 1)
     tile_kernel(const __grid_constant__ CUtensorMap in_map,
                 const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
@@ -606,6 +607,92 @@ __global__ void __launch_bounds__(NG * NW * 32, (CH >> 4) > 0 ? (CH >> 4) : 1)
     }
   }
   if (GATHER || lane == 0) bulk_wait_all();
+}
+
+// Shared-ring producer / consumer kernel (LINEAR blocks, one block per stage):
+// NC compute warps + 1 TMA producer warp per CTA, one CTA per SM, an S-stage ring
+// SHARED by the compute warps (tile i of the CTA -> stage i % S, warp i % NC).
+// The ring depth is decoupled from the warp count, which is what the 64x64 fp32
+// tiles need: packed (FFMA2) 64-point passes hold two rows / two columns per
+// lane (~200 registers), so only ~8 warps fit, and with the tile kernel's
+// per-warp rings each of them would need >= 2 private 16 KB stages.
+//   producer (lane 0): loads S tiles ahead; for each tile in order waits done[s],
+//     issues the TMA store, and refills the previous tile's stage once its store
+//     has been read (cp.async.bulk.wait_group.read 1)
+//   compute warp: waits full[s], row + column pass in place (packed pairs),
+//     fence.proxy.async, arrives done[s]
+template <typename T, int H, int W, int RC, int CC, bool COL_FIRST, int NC, int S>
+__global__ void __launch_bounds__((NC + 1) * 32, 1)
+    ring_kernel(const __grid_constant__ CUtensorMap in_map,
+                const __grid_constant__ CUtensorMap out_map, const __grid_constant__ Geom geom,
+                const __grid_constant__ KParams<T, W, H, RC, CC> prm) {
+  using L = TileLayout<T, H, W, 1>;
+  using RowOp = AxisOp<T, W, RC>;
+  using ColOp = AxisOp<T, H, CC>;
+  static_assert(!RowOp::kDense && !ColOp::kDense, "dense ops use the tile kernel");
+  static_assert(sizeof(T) == 4 && L::PH == 64 && W == 64, "packed pairs over 64 rows / columns");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGEB);
+  uint64_t* done = full + S;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], 1);
+    }
+    fence_mbar_init();
+    prefetch_map(&in_map);
+    prefetch_map(&out_map);
+  }
+  __syncthreads();
+  const int64_t G = gridDim.x;
+  const int64_t n = geom.ntiles > blockIdx.x ? (geom.ntiles - blockIdx.x + G - 1) / G : 0;
+  constexpr int GSQ = RowOp::kGainSq * ColOp::kGainSq;
+  if (warp == NC) {
+    if (lane == 0) {
+      auto load = [&](int64_t i) {
+        const int s = static_cast<int>(i % S);
+        mbar_arrive_expect_tx(&full[s], L::TILEB);
+        issue_tile_io<T, H, W, 1, MODE_LINEAR>(true, smem + s * L::STAGEB, &in_map, &full[s],
+                                               blockIdx.x + i * G, geom, 1);
+      };
+      for (int64_t i = 0; i < S && i < n; ++i) load(i);
+      for (int64_t i = 0; i < n; ++i) {
+        const int s = static_cast<int>(i % S);
+        mbar_wait(&done[s], static_cast<uint32_t>((i / S) & 1));
+        issue_tile_io<T, H, W, 1, MODE_LINEAR>(false, smem + s * L::STAGEB, &out_map, nullptr,
+                                               blockIdx.x + i * G, geom, 1);
+        bulk_commit();
+        if (i >= 1 && i - 1 + S < n) {  // tile i-1's stage: its store has been read
+          bulk_wait_read<1>();
+          load(i - 1 + S);
+        }
+      }
+      bulk_wait_all();
+    }
+    return;
+  }
+  for (int64_t i = warp; i < n; i += NC) {
+    const int s = static_cast<int>(i % S);
+    uint8_t* buf = smem + s * L::STAGEB;
+    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
+    if constexpr (!COL_FIRST) {
+      row_pass<T, H, W, 1, RC, 1, true>(buf, lane, prm.row, nullptr);
+      __syncwarp();
+      col_pass<T, H, W, 1, CC, GSQ, true>(buf, lane, prm.col, nullptr);
+    } else {
+      col_pass<T, H, W, 1, CC, 1, true>(buf, lane, prm.col, nullptr);
+      __syncwarp();
+      row_pass<T, H, W, 1, RC, GSQ, true>(buf, lane, prm.row, nullptr);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[s]);
+  }
 }
 
 }  // namespace dctadj

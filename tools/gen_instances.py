@@ -71,7 +71,15 @@ def tile_config(dtype: str, h: int, w: int, two_d: bool, col_first: bool = False
     stage = -(-tile // 1024) * 1024
     if two_d and dtype == "float" and (h, w) == (64, 64):
         givens = (rc & 15) == GIVENS or ((rc >> 4) & 15) == GIVENS
-        if givens or col_first:
+        if givens:
+            # band-6 pre (Givens): the shared-ring kernel -- 8 compute warps with
+            # packed 64-point passes (168 registers: 3 warps share an SMSP) + a TMA
+            # producer, 13 x 16 KB stages shared by the warps (ring_kernel, CH bit
+            # 3).  Measured (profiles/r02_tuning.md) fwd / inv 1.62 / 1.65 ms vs
+            # 1.82-1.87 / 1.75 for the two-warp scalar tile kernel; 7 warps at 188
+            # registers 1.77 / 1.70; one butterfly copy for both passes 2.31 / 1.96
+            return 1, 8, 13, ("RING", 1, 8)
+        if col_first:
             # 64-point vectors: two warps per tile, scalar lanes, 12 warps/SM
             # (the packed 64-column pass needs ~200 registers; measured faster)
             return p, 6, 2, ("NW", 2, 0)
@@ -162,7 +170,10 @@ EXPERIMENT = {
                (2, 4, 4, False, True, 0)],
     ("float", 64, 64): [(1, 6, 2, False, False, 0, 2), (1, 4, 3, False, False, 0, 2),
                (1, 5, 2, False, False, 0, 2), (1, 3, 4, False, False, 0, 2),
-               (2, 3, 2, False, False, 0, 4), (2, 2, 3, False, False, 0, 4)],
+               (2, 3, 2, False, False, 0, 4), (2, 2, 3, False, False, 0, 4),
+               # shared-ring kernel (CH bit 3): NC compute warps x S stages
+               (1, 7, 13, True, True, 8, 1), (1, 11, 13, True, True, 8, 1),
+               (1, 11, 14, True, True, 8, 1)],
 }
 EXPERIMENT_OPS = None  # filled below: the band-6 and sub-8 2-D ops
 # interleaved frame kernels (config 5): (P, NG, S); pair flags as the default
@@ -236,6 +247,8 @@ def instances():
         _, pc = pair_flags(dt, h, w, p, rc, cc)
         if isinstance(pr, tuple) and pr[0] == "NW":  # NW warps per tile, scalar lanes, CH bits
             final.append(inst[:11] + (False, False, 0, pr[2], pr[1]))
+        elif isinstance(pr, tuple) and pr[0] == "RING":  # ring kernel: packed rows + columns
+            final.append(inst[:11] + (True, True, 0, pr[2], pr[1]))
         else:
             final.append(inst[:11] + (pr and cc != ID, pc, 0, 0))
         if not TUNING:
