@@ -291,22 +291,36 @@ static void pack_band(const dctadj_axis* ax, bool transpose, int k, std::vector<
     }
 }
 
-// Lifting coefficients (tan(theta/2), sin(theta)) of a brick-wall schedule in
-// application order: layers 0..K-2 forward; for A^T the layers reversed with
-// negated angles (for even K the reversed layers keep the l%2 offsets).
-static void pack_givens(const dctadj_axis* ax, bool inverse, std::vector<double>& c) {
+// Scaled-rotation coefficients of a brick-wall Givens schedule (ST_GIVENS2,
+// butterfly.cuh) in application order -- layers 0..K-2 forward; for A^T the
+// layers reversed with negated angles (for even K they keep the l%2 offsets):
+// per rotation in application order (k1, k2) = (-t b / a, t a / b) with t =
+// tan(theta) and a, b the running scales of the pair, then the n final scales
+// (times gain when the stage trails the base: its 1/sqrt(n) is folded in).
+// false when some |cos(theta)| < kGivens2MinCos (large tan: the band then runs
+// as the matrix product or the dense composite).
+constexpr double kGivens2MinCos = 0.2;
+static bool pack_givens2(const dctadj_axis* ax, bool inverse, double gain, std::vector<double>& c) {
   const int n = ax->n, k = ax->taps;
   std::vector<int> start(k, 0);
   for (int l = 0; l + 1 < k; ++l) start[l + 1] = start[l] + givens_layer_rots(n, l);
+  std::vector<double> a(static_cast<size_t>(n), 1.0);
   c.clear();
-  for (int a = 0; a < k - 1; ++a) {
-    const int l = inverse ? k - 2 - a : a;
+  for (int s = 0; s < k - 1; ++s) {
+    const int l = inverse ? k - 2 - s : s;
     for (int r = 0; r < givens_layer_rots(n, l); ++r) {
       const double th = inverse ? -ax->givens[start[l] + r] : ax->givens[start[l] + r];
-      c.push_back(std::tan(0.5 * th));
-      c.push_back(std::sin(th));
+      const double co = std::cos(th), t = std::tan(th);
+      if (!(std::abs(co) >= kGivens2MinCos)) return false;
+      const int i = l % 2 + 2 * r;
+      c.push_back(-t * a[i + 1] / a[i]);
+      c.push_back(t * a[i] / a[i + 1]);
+      a[i] *= co;
+      a[i + 1] *= co;
     }
   }
+  for (int i = 0; i < n; ++i) c.push_back(a[i] * gain);
+  return true;
 }
 
 static void pack_sub(const dctadj_axis* ax, bool transpose, int k, std::vector<double>& c) {
@@ -326,11 +340,16 @@ static int plan_axis(const dctadj_axis* ax, bool inverse, bool force_dense, Axis
   const int bi = ax->base == DCTADJ_BASE_DCT2 ? ST_IDCT2 : ax->base == DCTADJ_BASE_DST3 ? ST_IDST3 : ST_DCT2;
   const int base = inverse ? bi : bf;
   int adj_stage = ST_NONE, k = 0;
+  // a band with its Givens schedule: scaled rotations (2 FMAs each); the stage
+  // trails the base for the inverse PRE / forward POST order, where the base's
+  // gain sqrt(n) is folded into the final scales
+  const bool adj_first = (ax->side == DCTADJ_SIDE_PRE) != inverse;
   if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps == 4 || ax->taps == 6) && ax->givens &&
-      ax->ngivens == givens_rots(ax->n, ax->taps)) {
-    adj_stage = ST_GIVENS;
+      ax->ngivens == givens_rots(ax->n, ax->taps) && !force_dense &&
+      pack_givens2(ax, inverse, adj_first ? 1.0 : 1.0 / std::sqrt(static_cast<double>(ax->n)),
+                   p->coef)) {
+    adj_stage = ST_GIVENS2;
     k = ax->taps;
-    pack_givens(ax, inverse, p->coef);
   } else if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps == 4 || ax->taps == 6)) {
     adj_stage = ST_BAND;
     k = ax->taps;
@@ -352,10 +371,11 @@ static int plan_axis(const dctadj_axis* ax, bool inverse, bool force_dense, Axis
   p->gain_sq = ax->n;
   if (adj_stage == ST_NONE)
     p->code = op_code(base);
-  else if ((ax->side == DCTADJ_SIDE_PRE) != inverse)  // fwd PRE or inv POST: adjustment first
+  else if (adj_first)  // fwd PRE or inv POST: adjustment first
     p->code = op_code(adj_stage, base, k);
   else
     p->code = op_code(base, adj_stage, k);
+  if (adj_stage == ST_GIVENS2 && !adj_first) p->gain_sq = 1;
   return ST_OK;
 }
 
@@ -1208,7 +1228,7 @@ static int run_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dc
       !plan_axis(h, false, false, &ph) && !plan_axis(v, false, false, &pv) &&
       !plan_axis(eh, false, true, &peh) && !plan_axis(ev, false, true, &pev) &&
       peh.code == op_code(ST_DENSE) && pev.code == op_code(ST_DENSE) && ph.code == pv.code) {
-    constexpr int kSub8 = op_code(ST_DCT2, ST_SUB, 8), kGiv6 = op_code(ST_GIVENS, ST_DST3, 6);
+    constexpr int kSub8 = op_code(ST_DCT2, ST_SUB, 8), kGiv6 = op_code(ST_GIVENS2, ST_DST3, 6);
     if (ph.code == kSub8 || ph.code == kGiv6) {
       Launch L;
       if ((rc = upload_dense(peh, dtype, st, &L.dense_row)) ||

@@ -214,7 +214,9 @@ enum Stage : int {
   ST_BAND = 5,   // K-tap band, coefficients packed [N][2K-1]
   ST_SUB = 6,    // leading KxK block, coefficients packed [K][K]
   ST_DENSE = 7,  // full N x N from shared memory
-  ST_GIVENS = 8, // K-tap band as K-1 brick-wall layers of plane rotations, lifting form
+  ST_GIVENS = 8, // (retired) the brick-wall layers in lifting form, 3 dependent FMAs each
+  ST_GIVENS2 = 9, // K-tap band as K-1 brick-wall layers of plane rotations (reference
+                  // design.py:225-243), scaled form: 2 FMAs each + one scale per sample
 };
 
 // Rotations in brick-wall layer l of an N-point band schedule (pairs (i, i+1),
@@ -247,8 +249,8 @@ struct StageCoef<T, N, K, ST_SUB> {
   static constexpr int count = K * K;
 };
 template <typename T, int N, int K>
-struct StageCoef<T, N, K, ST_GIVENS> {
-  static constexpr int count = 2 * givens_rots(N, K);  // (tan(theta/2), sin(theta)) per rotation
+struct StageCoef<T, N, K, ST_GIVENS2> {
+  static constexpr int count = 2 * givens_rots(N, K) + N;  // (k1, k2) per rotation, N scales
 };
 
 template <typename T, int N, int CODE>
@@ -260,9 +262,11 @@ struct AxisOp {
   static constexpr int NCOEF = NC1 + NC2;
   static constexpr bool kDense = (S1 == ST_DENSE) || (S2 == ST_DENSE);
   static constexpr bool kIdentity = (S1 == ST_NONE) && (S2 == ST_NONE);
-  // the base stages run unnormalized: gain sqrt(N) (removed once per launch)
+  // the base stages run unnormalized: gain sqrt(N) (removed once per launch) --
+  // except behind a trailing scaled-Givens stage, whose per-sample scales carry
+  // 1/sqrt(N) already (the host folds it in)
   static constexpr bool kBase = (S1 >= ST_DCT2 && S1 <= ST_IDST3) || (S2 >= ST_DCT2 && S2 <= ST_IDST3);
-  static constexpr int kGainSq = kBase ? N : 1;  // gain^2
+  static constexpr int kGainSq = (kBase && S2 != ST_GIVENS2) ? N : 1;  // gain^2
   struct Coef {
     T c[NCOEF > 0 ? NCOEF : 1];
   };
@@ -323,14 +327,16 @@ DA_DEV void run_stage(V (&v)[N], const typename Scalar<V>::type* __restrict__ cf
     }
 #pragma unroll
     for (int r = 0; r < K; ++r) v[r] = y[r];
-  } else if constexpr (S == ST_GIVENS) {
+  } else if constexpr (S == ST_GIVENS2) {
     // y = L_{K-2} ... L_0 x, each layer index-disjoint rotations
     //   x_i' = c x_i - s x_j,  x_j' = s x_i + c x_j   (reference design.py:137-147)
-    // in lifting form, 3 FMAs per rotation with t = tan(theta/2):
-    //   a = x_i - t x_j;  x_j' = x_j + s a;  x_i' = a - t x_j'
-    // (7.5 FMAs per sample for K = 6 against 11 for the band product).  The
-    // host packs the layers in application order (reversed, angles negated,
-    // for A^T).
+    // with cos(theta) factored out and carried as a per-sample
+    // scale: the held values are u = a U, v = b V (a, b known per sample), and
+    //   U' = U + k1 V,  V' = V + k2 U,  k1 = -tan(theta) b / a,  k2 = tan(theta) a / b
+    // (both scales times cos(theta)) -- 2 independent FMAs per rotation instead of
+    // the lifting form's 3 dependent ones.  The host tracks the scales through the
+    // schedule (|cos theta| >= 0.2, else the band runs another way) and appends
+    // them; one multiply per sample at the end restores the rotated values.
 #pragma unroll
     for (int l = 0; l < K - 1; ++l) {
 #pragma unroll
@@ -339,13 +345,14 @@ DA_DEV void run_stage(V (&v)[N], const typename Scalar<V>::type* __restrict__ cf
 #pragma unroll
         for (int m = 0; m < l; ++m) q += givens_layer_rots(N, m);
         q += (i - l % 2) / 2;
-        const auto t = cf[2 * q], sn = cf[2 * q + 1];
-        const V a = fnmac(v[i + 1], t, v[i]);
-        const V b = fmac(a, sn, v[i + 1]);
-        v[i] = fnmac(b, t, a);
-        v[i + 1] = b;
+        const V u = v[i], w = v[i + 1];
+        v[i] = fmac(w, cf[2 * q], u);
+        v[i + 1] = fmac(u, cf[2 * q + 1], w);
       }
     }
+    constexpr int R = givens_rots(N, K);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = mul(v[i], cf[2 * R + i]);
   } else if constexpr (S == ST_DENSE) {
     V y[N];
 #pragma unroll

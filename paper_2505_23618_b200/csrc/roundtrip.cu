@@ -72,10 +72,10 @@ int launch_roundtrip(const RtArgs& a) {
 // op codes (butterfly.cuh): stage1 | stage2 << 4 | k << 8
 constexpr int kSubF = op_code(ST_DCT2, ST_SUB, 8);      // sub-block post, forward
 constexpr int kSubI = op_code(ST_SUB, ST_IDCT2, 8);     // sub-block post, inverse
-constexpr int kG7F = op_code(ST_GIVENS, ST_DST3, 6);    // band-6 pre DST-7, forward
-constexpr int kG7I = op_code(ST_IDST3, ST_GIVENS, 6);   // band-6 pre DST-7, inverse
-constexpr int kG8F = op_code(ST_GIVENS, ST_IDCT2, 6);   // band-6 pre DCT-8 (DCT-3 base)
-constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS, 6);
+constexpr int kG7F = op_code(ST_GIVENS2, ST_DST3, 6);    // band-6 pre DST-7, forward
+constexpr int kG7I = op_code(ST_IDST3, ST_GIVENS2, 6);   // band-6 pre DST-7, inverse
+constexpr int kG8F = op_code(ST_GIVENS2, ST_IDCT2, 6);   // band-6 pre DCT-8 (DCT-3 base)
+constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS2, 6);
 
 // TUNE(...) keeps a measured-slower tuning variant in the table only when the
 // library is built with DCTADJ_TUNING=1 (tools/gen_instances.py, Makefile).

@@ -728,3 +728,39 @@ def test_dense_tc64_repeat_and_streams():
         y1 = pipeline.forward_adjusted_2d(th, tv, x)
     s.synchronize()
     assert torch.equal(y1, y0)
+
+
+@pytest.mark.parametrize("n", [16, 32, 64])
+@pytest.mark.parametrize("big", [False, True])
+def test_givens_scaled_rotations_and_large_angle_fallback(n, big):
+    """Band pre-adjustments run their Givens schedule as scaled rotations (2 FMAs
+    each, csrc/butterfly.cuh ST_GIVENS2) when every |cos theta| >= 0.2; a schedule
+    with a steeper rotation falls back to the band product / dense composite.  Both
+    must match the oracle (the realized matrix) in fp64 and fp32, 1-D and 2-D,
+    forward and inverse."""
+    import dataclasses
+
+    from paper_2505_23618_b200.design import givens_to_matrix
+
+    adj = matio.load_designed(f"band6_pre_dst3_dst7_n{n}")
+    if big:  # one rotation at 84 degrees (cos 0.10): below the scaled form's bound
+        th = adj.schedule.angles().copy()
+        th[len(th) // 3] = np.radians(84.0)
+        sch = adj.schedule.with_angles(th)
+        adj = dataclasses.replace(adj, schedule=sch, realized=givens_to_matrix(sch))
+    t = pipeline.make_adjusted_transform(adj)
+    ax = oaxis(adj)
+    rng = np.random.default_rng(n + 7 * big)
+    x = rng.standard_normal((40, n, n)) * 24
+    v = rng.standard_normal((100, n)) * 24
+    for dtype, tol in ((torch.float64, F64_TOL), (torch.float32, F32_TOL)):
+        xd = dev(x, dtype)
+        y = pipeline.forward_adjusted_2d(t, t, xd)
+        assert rel_err(y.cpu().numpy(), O.adjusted_2d(ax, ax, x)) < tol
+        xr = pipeline.inverse_adjusted_2d(t, t, y)
+        assert rel_err(xr.cpu().numpy(), x) < 10 * tol
+        y1 = pipeline.forward_adjusted(t, dev(v, dtype))
+        assert rel_err(y1.cpu().numpy(), O.adjusted_1d(ax, v)) < tol
+        x1 = pipeline.inverse_adjusted(t, y1)
+        assert rel_err(x1.cpu().numpy(), O.adjusted_1d(ax, y1.cpu().numpy().astype(np.float64),
+                                                      inverse=True)) < tol

@@ -19,7 +19,9 @@ NSHARDS_COLD = 12  # gen/inst_cNN.cu: 1-D primitives, dense composites, copy (no
 # DCTADJ_TUNING=1; the shipped library holds the defaults alone.
 TUNING = os.environ.get("DCTADJ_TUNING", "0") not in ("", "0")
 
-NONE, DCT2, IDCT2, DST3, IDST3, BAND, SUB, DENSE, GIVENS = range(9)
+NONE, DCT2, IDCT2, DST3, IDST3, BAND, SUB, DENSE, GIVENS_LIFT, GIVENS = range(10)
+# GIVENS: the band's Givens schedule as scaled rotations (ST_GIVENS2, 2 FMAs per
+# rotation); the lifting form (ST_GIVENS, 3 FMAs) is no longer instantiated
 
 
 def code(s1, s2=NONE, k=0):
