@@ -626,6 +626,79 @@ static int stream_sched_counter(cudaStream_t st, unsigned long long** out) {
   return ST_OK;
 }
 
+// ------------------------------------------------ cross-launch overlap (PDL)
+// Every tile / ring / round-trip grid triggers its dependents at entry, so the
+// next grid of the stream is scheduled while this one drains.  Normally the next
+// grid then waits (griddepcontrol.wait) before touching memory.  When its byte
+// ranges overlap none of the launches that may still be running on the stream
+// -- every launch since the last one that waited at entry -- it may skip that
+// wait (Geom::early) and wait at exit instead: its loads and passes fill the
+// previous grid's tail, yet it never completes before it.  Ranges are per
+// (device, stream); any other PDL-triggering launch poisons the record.  Other
+// stream work (copies, events, kernels launched without the PDL attribute) is
+// ordered normally by CUDA, which only makes the record conservative.
+// DCTADJ_PDL_EARLY=0 disables the overlap.
+namespace {
+struct PdlLaunch {
+  ByteRange in, out1, out2;
+};
+struct PdlStream {
+  int device;
+  cudaStream_t stream;
+  bool poison;
+  std::vector<PdlLaunch> live;  // since (and including) the last entry-waiting launch
+};
+std::mutex g_pdl_mu;
+std::vector<PdlStream> g_pdl;
+constexpr size_t kPdlMaxLive = 32;
+
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("DCTADJ_PDL_EARLY");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+bool overlaps(ByteRange a, ByteRange b) {
+  if (!a.p || !b.p || a.n == 0 || b.n == 0) return false;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a.p), b0 = reinterpret_cast<uintptr_t>(b.p);
+  return a0 < b0 + b.n && b0 < a0 + a.n;
+}
+PdlStream& pdl_stream(cudaStream_t st) {
+  int device = 0;
+  cudaGetDevice(&device);
+  for (auto& e : g_pdl)
+    if (e.device == device && e.stream == st) return e;
+  g_pdl.push_back({device, st, true, {}});  // unknown history: the first launch waits
+  return g_pdl.back();
+}
+}  // namespace
+
+bool pdl_early(cudaStream_t st, ByteRange in, ByteRange out1, ByteRange out2) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  PdlStream& r = pdl_stream(st);
+  bool ok = pdl_enabled() && !r.poison && r.live.size() < kPdlMaxLive;
+  for (size_t i = 0; ok && i < r.live.size(); ++i) {
+    const PdlLaunch& p = r.live[i];
+    // read-after-write, write-after-read, write-after-write
+    if (overlaps(in, p.out1) || overlaps(in, p.out2) || overlaps(out1, p.in) ||
+        overlaps(out1, p.out1) || overlaps(out1, p.out2) || overlaps(out2, p.in) ||
+        overlaps(out2, p.out1) || overlaps(out2, p.out2))
+      ok = false;
+  }
+  if (!ok) r.live.clear();
+  r.poison = false;
+  r.live.push_back({in, out1, out2});
+  return ok;
+}
+
+void pdl_poison(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  PdlStream& r = pdl_stream(st);
+  r.poison = true;
+  r.live.clear();
+}
+
 // fused config-5 launch: the adjusted transform's output, packed coefficients
 // (already in fp32) and the per-frame error accumulator
 struct FusedArgs {
@@ -711,6 +784,7 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  pdl_poison(a.stream);
   DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm, adj_map, kp));
   if (trace_file) {
     std::vector<unsigned long long> h(kTcTraceTiles * kTcTraceEv + 2 * kTcTraceCtas);
@@ -784,6 +858,7 @@ static int launch_frames_exact(const LaunchArgs& a, int64_t nblocks, int tiles_y
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  pdl_poison(a.stream);
   DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm, adj_map, kp));
   return ST_OK;
 }
@@ -819,6 +894,7 @@ static int launch_dense_tc64(const LaunchArgs& a, int64_t nblocks) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  pdl_poison(a.stream);
   DA_CUDA(cudaLaunchKernelEx(&cfg, kern, in_map, out_map, g, prm));
   return ST_OK;
 }

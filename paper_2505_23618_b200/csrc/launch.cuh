@@ -51,6 +51,17 @@ int encode_tensor_map(CUtensorMap* map, int dtype, int rank, const uint64_t* dim
                       const uint64_t* strides_bytes, const uint32_t* box, int box_row_bytes,
                       void* base);
 int num_sms_cached();
+// Cross-launch overlap bookkeeping (abi.cu): may a launch reading [in, in + nin)
+// and writing the two output ranges skip the entry wait on the previous grid of
+// the stream (it overlaps none of the ranges of the launches that may still be
+// running there)?  Records the launch either way.  pdl_poison: a launch whose
+// ranges are not tracked -- the next launch on the stream waits at entry.
+struct ByteRange {
+  const void* p;
+  size_t n;
+};
+bool pdl_early(cudaStream_t st, ByteRange in, ByteRange out1, ByteRange out2 = {nullptr, 0});
+void pdl_poison(cudaStream_t st);
 void set_last_error(const char* fmt, ...);
 
 // One-time launch setup of a kernel on the current device (dynamic shared
@@ -147,6 +158,12 @@ int launch_tile(const LaunchArgs& a) {
   if (g.ntiles == 0) return ST_OK;
   g.dense_row = a.dense_row;
   g.dense_col = a.dense_col;
+  if constexpr (IN_MODE == MODE_LINEAR && OUT_MODE == MODE_LINEAR) {
+    const size_t bytes = static_cast<size_t>(g.ntiles) * L::PH * W * sizeof(T);
+    g.early = pdl_early(a.stream, {a.in, bytes}, {a.out, bytes}) ? 1 : 0;
+  } else {
+    pdl_poison(a.stream);
+  }
 
   // the LINEAR side of a frame launch holds ntiles whole blocks
   LaunchArgs la = a;

@@ -22,6 +22,12 @@ int launch_roundtrip(const RtArgs& a) {
     g.nblocks = g.ntiles * P;
   }
   if (g.ntiles == 0) return ST_OK;
+  if constexpr (MODE == MODE_LINEAR) {
+    const size_t bytes = static_cast<size_t>(a.rows) * W * sizeof(T);
+    g.early = pdl_early(a.stream, {a.in, bytes}, {a.y, bytes}, {a.xr, bytes}) ? 1 : 0;
+  } else {
+    pdl_poison(a.stream);
+  }
   LaunchArgs la;
   la.rows = a.rows;
   CUtensorMap in_map, y_map, xr_map;

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
   constexpr int GSQI = RowI::kGainSq * ColI::kGainSq;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!geom.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // see Geom::early
   asm volatile("griddepcontrol.launch_dependents;" :::);
   constexpr int GT = NW * 32;
   static_assert(NW == 1 || NG <= 15, "named barriers 1..15");
@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(NG * NW * 32, MINB)
     }
   }
   if (GATHER || lane == 0) bulk_wait_all();
+  if (geom.early) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 }  // namespace dctadj

@@ -201,6 +201,10 @@ struct Geom {
   const void* dense_row;  // device N x N (T) for ST_DENSE row op
   const void* dense_col;  // device N x N (T) for ST_DENSE column op
   const int64_t* offsets; // GATHER: element offset of each block (device)
+  int32_t early;          // 1: independent of every launch still in flight on the stream
+                          // (host-checked, pdl_early): skip the entry griddepcontrol.wait
+                          // and wait at exit instead, so this grid's loads and passes
+                          // overlap the previous grid's tail but it never completes first
 };
 
 template <typename T, int W, int H, int RC, int CC>
@@ -455,9 +459,10 @@ __global__ void __launch_bounds__(NG * NW * 32, (CH >> 4) > 0 ? (CH >> 4) : 1)
   // (pointer arithmetic, not an integer round trip, keeps the shared address space)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // Programmatic dependent launch: this grid may have been scheduled while the
-  // previous kernel in the stream drains; wait for it before touching memory,
-  // and let the next kernel get scheduled as our CTAs retire.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // previous kernel in the stream drains; wait for it before touching memory
+  // (unless the host proved the two independent: geom.early), and let the next
+  // kernel get scheduled as our CTAs retire.
+  if (!geom.early) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
   // `lane`: thread index within the group (0 .. NW*32-1)
   const int grp = threadIdx.x / GT, lane = threadIdx.x % GT;
@@ -607,6 +612,7 @@ __global__ void __launch_bounds__(NG * NW * 32, (CH >> 4) > 0 ? (CH >> 4) : 1)
     }
   }
   if (GATHER || lane == 0) bulk_wait_all();
+  if (geom.early) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Shared-ring producer / consumer kernel (LINEAR blocks, one block per stage):
@@ -635,7 +641,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGEB);
   uint64_t* done = full + S;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!geom.early) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -674,6 +680,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
       }
       bulk_wait_all();
     }
+    if (geom.early) asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
   for (int64_t i = warp; i < n; i += NC) {
@@ -693,6 +700,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&done[s]);
   }
+  if (geom.early) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 }  // namespace dctadj
