@@ -768,7 +768,7 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   constexpr int NG = kDenseTcGroups;
   constexpr int NTHR = (4 * NG + 3) * 32;
   auto kern = dense_tc_kernel<S, IN_MODE, OUT_MODE, FRC, FCC, NG>;
-  const size_t smem = 1024 + S * 16384 + NG * 16384 + 16384 + (2 * S + 4 * NG) * 8 + (S + 1) * 8 +
+  const size_t smem = 1024 + S * 16384 + NG * 16384 + 16384 + (2 * S + 4 * NG) * 8 + (S + NG) * 8 +
                       NG * 16 * 8 + 16;
   static std::atomic<int> setup[kMaxDevices];  // per instantiation and device
   if (!kernel_blocks_per_sm(kern, NTHR, smem, setup, "dense_tc_kernel")) return ST_ERR_CUDA;

@@ -242,8 +242,9 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
   uint64_t* a2_ready = d1_done + NGRP;
   uint64_t* d2_done = a2_ready + NGRP;
   int64_t* tile_id = reinterpret_cast<int64_t*>(d2_done + NGRP);  // per ring stage; -1 = end
-  volatile int64_t* total_k = tile_id + S;  // tiles this CTA got (-1 until known)
-  double* red = reinterpret_cast<double*>(tile_id + S + 1);  // NGRP x 4 warps x 4 (fused)
+  // per group: the tile index of its end marker (set before its ready arrivals)
+  volatile int64_t* mma_end = tile_id + S;
+  double* red = reinterpret_cast<double*>(tile_id + S + NGRP);  // NGRP x 4 warps x 4 (fused)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red + NGRP * 16);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
       mbar_init(&a2_ready[g], 1);
       mbar_init(&d2_done[g], 1);
     }
-    *total_k = -1;
+    for (int g = 0; g < NGRP; ++g) mma_end[g] = INT64_MAX;
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -311,7 +312,6 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
         chunk = gridDim.x + static_cast<int64_t>(nxt);
         if (chunk * CH < ntiles) nxt = atomicAdd(prm.sched, 1ull);
       }
-      *total_k = k;
       asm volatile("griddepcontrol.launch_dependents;" :::);
       for (int j = 0; j < NGRP; ++j, ++k) {  // one end marker per epilogue group
         const int s = static_cast<int>(k % S);
@@ -332,15 +332,19 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
       for (int64_t k = 0;; ++k) {
         const int g = static_cast<int>(k % NGRP);
         const uint32_t par = static_cast<uint32_t>((k / NGRP) & 1);
-        bool ok;
-        while (!(ok = mbar_test(&ready[g], par))) {  // poll: try_wait's suspend adds latency
-          const int64_t tot = *total_k;
-          if (tot >= 0 && k >= tot) break;
-          // the polling warp shares an SM sub-partition with epilogue warps: backing
-          // off returns their issue slots (the fused config-5 kernel is issue-bound)
-          if (prm.spin_ns > 0) __nanosleep(prm.spin_ns);
+        // the dense kernel polls (try_wait's suspend adds latency to a latency-bound
+        // pipeline); the fused one is issue-bound and blocks instead, returning the
+        // issue slots of the SM sub-partitions it shares with epilogue warps
+        if constexpr (FUSED) {
+          mbar_wait(&ready[g], par);
+        } else {
+          while (!mbar_test(&ready[g], par)) {
+            if (prm.spin_ns > 0) __nanosleep(prm.spin_ns);
+          }
         }
-        if (!ok) break;
+        // group g met its end marker at tile index k: its earlier arrivals are all
+        // consumed (it finished tile k - NGRP, both passes, before reaching it)
+        if (k >= mma_end[g]) break;
         if (pass1 && prm.trace && blockIdx.x == 0 && k < kTcTraceTiles)
           prm.trace[k * kTcTraceEv + 7] = clock64();
         tc::fence_after();
@@ -401,7 +405,14 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
         }
         prev_s = s;
       }
-      if (t < 0) break;
+      if (t < 0) {  // end marker: release the MMA issuers waiting for tile k
+        if (leader) {
+          mma_end[g] = k;
+          mbar_arrive(&a1_ready[g]);
+          mbar_arrive(&a2_ready[g]);
+        }
+        break;
+      }
       ev(k, 1);
 #pragma unroll
       for (int i = 0; i < 32; ++i)
@@ -446,7 +457,7 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
       group_bar();
       if (leader) mbar_arrive(&a2_ready[g]);
       if constexpr (FUSED) {  // (the barrier above also closed the row pass)
-        col_pass<float, 32, 32, 4, FCC, GSQ, false, 128, true>(x, gl, kp.col, nullptr);
+        col_pass<float, 32, 32, 4, FCC, GSQ, false, 128, true, true>(x, gl, kp.col, nullptr);
         fence_proxy_async_smem();
         group_bar();
         if (leader) {

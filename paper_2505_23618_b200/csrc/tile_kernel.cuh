@@ -165,6 +165,20 @@ struct TileLayout {
     const uint32_t a = rho * BRB + off;
     return b * BOXB + (a ^ (((a >> 7) & SWZ_MASK) << 4));
   }
+  // Column walks: rows rho0 + i * STEP at one byte offset.  The swizzle term of
+  // every TMA pattern above repeats every 8 rows, so addr(rho0 + i STEP, byte) =
+  // base[i % M] + i * STEP * BRB with M = 8 / gcd(STEP, 8): a per-lane base
+  // register plus an immediate, no integer work per element once i is unrolled.
+  template <int STEP>
+  struct Col {
+    static constexpr int M = 8 / (STEP % 8 == 0 ? 8 : STEP % 4 == 0 ? 4 : STEP % 2 == 0 ? 2 : 1);
+    uint32_t base[M];
+    DA_DEV Col(uint32_t rho0, uint32_t byte) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) base[m] = addr(rho0 + m * STEP, byte) - m * STEP * BRB;
+    }
+    DA_DEV uint32_t operator()(int i) const { return base[i % M] + i * STEP * BRB; }
+  };
 };
 
 // LINEAR: super-tile t = rows [t*P*H, (t+1)*P*H) of a [rows, W] view.
@@ -391,40 +405,45 @@ DA_DEV void row_pass(uint8_t* buf, int lane, const typename AxisOp<T, W, RC>::Co
 
 // Column pass: lane owns a column (PAIR: two adjacent columns read as one
 // 8-byte word, packed as f2 lanes).  Conflict-free under the swizzle.
+// COLADDR: walk the column with TileLayout::Col's precomputed bases (a register
+// plus an immediate per element) instead of recomputing each swizzled address --
+// fewer integer instructions, which pays in the issue-bound fused config-5
+// kernel; measured neutral (block-major) to 6 % slower (interleaved frame
+// kernels) in the tile kernels, which keep the per-element form.
 template <typename T, int H, int W, int P, int CC, int GSQ, bool PAIR, int GT = 32,
-          bool IL = false>
+          bool IL = false, bool COLADDR = false>
 DA_DEV void col_pass(uint8_t* buf, int lane, const typename AxisOp<T, H, CC>::Coef& cf,
                      const T* dense) {
   using L = TileLayout<T, H, W, P>;
   // tile row of (block p, block row i): block-major, or row-interleaved (IL)
-  auto row = [](uint32_t p, uint32_t i) { return IL ? i * P + p : p * H + i; };
   constexpr int COLS_PER_IT = PAIR ? 2 * GT : GT;
   static_assert((P * W) % COLS_PER_IT == 0, "column pass must cover whole warps");
 #pragma unroll 1
   for (int it = 0; it < (P * W) / COLS_PER_IT; ++it) {
     const int kappa = it * COLS_PER_IT + (PAIR ? 2 : 1) * lane;
     const uint32_t p = kappa / W, c = kappa % W;
-    const uint32_t byte = c * sizeof(T);
+    // tile row of (block p, block row i): block-major, or row-interleaved (IL)
+    const typename L::template Col<IL ? P : 1> col(IL ? p : p * H, c * sizeof(T));
+    auto at = [&](int i) -> uint32_t {
+      return COLADDR ? col(i) : L::addr(IL ? i * P + p : p * H + i, c * sizeof(T));
+    };
     if constexpr (!PAIR) {
       T v[H];
 #pragma unroll
-      for (int i = 0; i < H; ++i)
-        v[i] = *reinterpret_cast<const T*>(buf + L::addr(row(p, i), byte));
+      for (int i = 0; i < H; ++i) v[i] = *reinterpret_cast<const T*>(buf + at(i));
       apply_axis<T, H, CC>(v, cf, dense);
       scale_out<T, H, GSQ>(v);
 #pragma unroll
-      for (int i = 0; i < H; ++i) *reinterpret_cast<T*>(buf + L::addr(row(p, i), byte)) = v[i];
+      for (int i = 0; i < H; ++i) *reinterpret_cast<T*>(buf + at(i)) = v[i];
     } else {
       static_assert(sizeof(T) == 4, "packed columns are fp32 pairs");
       f2 v[H];
 #pragma unroll
-      for (int i = 0; i < H; ++i)
-        v[i].v = *reinterpret_cast<const float2*>(buf + L::addr(row(p, i), byte));
+      for (int i = 0; i < H; ++i) v[i].v = *reinterpret_cast<const float2*>(buf + at(i));
       apply_axis<f2, H, CC>(v, cf, dense);
       scale_out<f2, H, GSQ>(v);
 #pragma unroll
-      for (int i = 0; i < H; ++i)
-        *reinterpret_cast<float2*>(buf + L::addr(row(p, i), byte)) = v[i].v;
+      for (int i = 0; i < H; ++i) *reinterpret_cast<float2*>(buf + at(i)) = v[i].v;
     }
   }
 }
