@@ -214,6 +214,14 @@ int32_t dctadj_kernel_count(void);
 /* the device cache of dense matrices (composites, exact comparison transforms):
  * entries held and entries pinned by calls still in flight (0 between calls) */
 int dctadj_dense_cache_state(int32_t* entries, int32_t* pinned);
+/* The cross-launch overlap rule, as the launchers apply it (no device work):
+ * would a launch on `stream` reading [in, in + in_bytes) and writing
+ * [out, out + out_bytes) skip its entry wait on the previous grid -- 1 yes, 0 no
+ * -- given every launch recorded there since the last one that waited?  The
+ * probe is recorded like a launch.  poison != 0 instead records a launch whose
+ * ranges are unknown (the next launch waits).  Returns 0 / 1, or < 0 on error. */
+int dctadj_pdl_probe(void* stream, const void* in, uint64_t in_bytes, const void* out,
+                     uint64_t out_bytes, int32_t poison);
 /* 1 when the library was built with DCTADJ_TUNING=1 (measured-slower tuning
  * variants selectable by DCTADJ_VARIANT / DCTADJ_RT_VARIANT), else 0 */
 int32_t dctadj_tuning_build(void);

@@ -91,6 +91,7 @@ SIGNATURES = {
     "dctadj_kernel_count": [],
     "dctadj_dense_cache_state": [ctypes.POINTER(_I32), ctypes.POINTER(_I32)],
     "dctadj_tuning_build": [],
+    "dctadj_pdl_probe": [_P, _P, ctypes.c_uint64, _P, ctypes.c_uint64, _I32],
 }
 
 _lib = None

@@ -1971,6 +1971,16 @@ int dctadj_dense_cache_state(int32_t* entries, int32_t* pinned) {
   dense_cache_state(entries, pinned);
   return ST_OK;
 }
+int dctadj_pdl_probe(void* stream, const void* in, uint64_t in_bytes, const void* out,
+                     uint64_t out_bytes, int32_t poison) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (poison) {
+    pdl_poison(st);
+    return 0;
+  }
+  return pdl_early(st, {in, static_cast<size_t>(in_bytes)}, {out, static_cast<size_t>(out_bytes)})
+             ? 1 : 0;
+}
 int32_t dctadj_tuning_build(void) {
 #ifdef DCTADJ_TUNING
   return 1;
