@@ -983,6 +983,8 @@ def _brief(r: dict) -> dict:
     g = r["gate"]
     out = {"workload": r["workload"], "value": r["value"], "ms_per_step": r["ms_per_step"],
            "frac": r["roofline"]["frac"], "kernel": r["roofline"]["kernel"],
+           "traffic": r["roofline"]["traffic"],
+           "algorithmic_bytes_per_launch": r["roofline"]["algorithmic_bytes_per_launch"],
            "avg_launch_ms": r["roofline"]["avg_launch_ms"],
            "per_launch_ms": r["roofline"]["per_launch_ms"],
            "gate": {k: (v if not isinstance(v, dict) else
