@@ -656,6 +656,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
   using ColOp = AxisOp<T, H, CC>;
   static_assert(!RowOp::kDense && !ColOp::kDense, "dense ops use the tile kernel");
   static_assert(sizeof(T) == 4 && L::PH == 64 && W == 64, "packed pairs over 64 rows / columns");
+  static_assert(S >= NC, "the stage hand-off below relies on S >= NC");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::STAGEB);
@@ -704,8 +705,20 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
   }
   for (int64_t i = warp; i < n; i += NC) {
     const int s = static_cast<int>(i % S);
+    const int64_t k = i / S;  // this is the k-th use of stage s
     uint8_t* buf = smem + s * L::STAGEB;
-    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
+    // A parity wait cannot tell phase k-1 from phase k+1.  Stage s's previous tile
+    // (i - S) belongs to ANOTHER warp, so nothing this warp did orders it before
+    // tile i: if its TMA load completed after the later-issued load of this warp's
+    // previous tile (i - NC), full[s] would still be at phase k-1 here and the
+    // parity-k wait would pass on the stale phase.  Waiting first for done[s] of
+    // tile i - S (phase k-1) closes that: tile i - 2S is always consumed by now
+    // (the producer issued load(i - NC) after done(i - NC - S + 1), and
+    // i - NC - S + 1 > i - 2S since S >= NC), so done[s] is at phase k-1 or later
+    // and this wait is exact; after it, full[s] is at phase k or k+1, and so is
+    // the wait below.
+    if (k >= 1) mbar_wait(&done[s], static_cast<uint32_t>((k - 1) & 1));
+    mbar_wait(&full[s], static_cast<uint32_t>(k & 1));
     if constexpr (!COL_FIRST) {
       row_pass<T, H, W, 1, RC, 1, true>(buf, lane, prm.row, nullptr);
       __syncwarp();

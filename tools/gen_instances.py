@@ -276,11 +276,6 @@ def instances():
             for k, ex in enumerate(EXPERIMENT[(dt, h, w)], start=1):
                 pp, nng, ss, pr, pc, ch = ex[:6]
                 nw = ex[6] if len(ex) > 6 else 1
-                if ch & 8 and rc in (code(DCT2, SUB, 8), code(SUB, IDCT2, 8)):
-                    # ring shapes other than the shipped 8 x 13 gave wrong results / hangs on
-                    # the sub-8 post inverse in tuning builds (profiles/r02_tuning.md):
-                    # ring variants are built for the Givens ops only
-                    continue
                 final.append((dt, h, w, pp, rc, cc, cf, im, om, nng, ss, pr, pc, k, ch, nw))
     return final
 
