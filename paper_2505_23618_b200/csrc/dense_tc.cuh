@@ -224,6 +224,10 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
   using ColOp = AxisOp<float, 32, FCC>;
   static_assert(!FUSED || (!RowOp::kDense && !ColOp::kDense), "fused ops are the fast paths");
   static_assert(NGRP * 128 <= 512, "TMEM columns");
+  // every use of ring stage s then belongs to the same group (tiles k = g mod NGRP,
+  // stage k mod S), which waited the stage's previous phase itself: the parity
+  // waits on full[s] are exact (shared stages need the hand-off of ring_kernel)
+  static_assert(S % NGRP == 0, "ring stages per epilogue group");
   using L = TileLayout<float, 32, 32, 4>;  // 128 rows x 128 B, SW128
   static_assert(L::TILEB == 16384 && L::STAGEB == 16384, "4 blocks of 32x32 fp32");
   extern __shared__ __align__(1024) uint8_t smem_raw[];

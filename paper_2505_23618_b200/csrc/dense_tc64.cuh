@@ -197,6 +197,11 @@ __global__ void __launch_bounds__(kTc64Threads, 1)
       const uint32_t gp = static_cast<uint32_t>((k / NGRP) & 1);
       const uint8_t* x = stages + s * 32768;
       uint32_t v[64];
+      // stage s's previous tile (k - S) belongs to the other group (S = 3, 2 groups):
+      // wait for its release first, or a parity wait on full[s] could pass on the
+      // stale phase if that older load completed after this group's previous one
+      // (ring_kernel in tile_kernel.cuh has the full argument)
+      if (k >= S) mbar_wait(&empty[s], static_cast<uint32_t>(((k / S) - 1) & 1));
       mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
       const int64_t t = tile_id[s];
       if (t < 0) break;

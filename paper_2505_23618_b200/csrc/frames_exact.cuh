@@ -206,6 +206,9 @@ __global__ void __launch_bounds__(kFxThreads, 1)
     for (int64_t j = 0;; ++j) {
       const int64_t k = m + NT * j;
       const int s = static_cast<int>(k % S);
+      // the stage's previous tile belongs to other consumers: wait for its release
+      // before the parity wait on full[s] (ring_kernel in tile_kernel.cuh)
+      if (k >= S) mbar_wait(&empty[s], static_cast<uint32_t>(((k / S) - 1) & 1));
       mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
       const int64_t t = tile_id[s];
       if (t < 0) break;
@@ -292,6 +295,7 @@ __global__ void __launch_bounds__(kFxThreads, 1)
       const int64_t k = g + NG * i;
       const int u = static_cast<int>(i & 1);
       const int s = static_cast<int>(k % S);
+      if (k >= S) mbar_wait(&empty[s], static_cast<uint32_t>(((k / S) - 1) & 1));  // as above
       mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
       const int64_t t = tile_id[s];
       if (t < 0) {  // release the MMA issuers waiting for this tile index
