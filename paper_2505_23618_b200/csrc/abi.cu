@@ -21,6 +21,7 @@
 #ifdef DCTADJ_TUNING
 #include "frames_exact.cuh"
 #endif
+#include "givens_pack.h"
 #include "launch.cuh"
 #include "roundtrip.cuh"
 
@@ -187,6 +188,9 @@ struct AxisPlan {
   int code = 0;
   int gain_sq = 1;
   std::vector<double> coef;   // packed band / sub-block coefficients (fp64)
+  // the same for fp64 kernels where their base form differs from fp32's (a Givens
+  // stage behind a deferred-scale base, butterfly.cuh deferred_policy); else empty
+  std::vector<double> coef64;
   std::vector<double> dense;  // n x n for ST_DENSE
 };
 
@@ -291,36 +295,11 @@ static void pack_band(const dctadj_axis* ax, bool transpose, int k, std::vector<
     }
 }
 
-// Scaled-rotation coefficients of a brick-wall Givens schedule (ST_GIVENS2,
-// butterfly.cuh) in application order -- layers 0..K-2 forward; for A^T the
-// layers reversed with negated angles (for even K they keep the l%2 offsets):
-// per rotation in application order (k1, k2) = (-t b / a, t a / b) with t =
-// tan(theta) and a, b the running scales of the pair, then the n final scales
-// (times gain when the stage trails the base: its 1/sqrt(n) is folded in).
-// false when some |cos(theta)| < kGivens2MinCos (large tan: the band then runs
-// as the matrix product or the dense composite).
-constexpr double kGivens2MinCos = 0.2;
-static bool pack_givens2(const dctadj_axis* ax, bool inverse, double gain, std::vector<double>& c) {
-  const int n = ax->n, k = ax->taps;
-  std::vector<int> start(k, 0);
-  for (int l = 0; l + 1 < k; ++l) start[l + 1] = start[l] + givens_layer_rots(n, l);
-  std::vector<double> a(static_cast<size_t>(n), 1.0);
-  c.clear();
-  for (int s = 0; s < k - 1; ++s) {
-    const int l = inverse ? k - 2 - s : s;
-    for (int r = 0; r < givens_layer_rots(n, l); ++r) {
-      const double th = inverse ? -ax->givens[start[l] + r] : ax->givens[start[l] + r];
-      const double co = std::cos(th), t = std::tan(th);
-      if (!(std::abs(co) >= kGivens2MinCos)) return false;
-      const int i = l % 2 + 2 * r;
-      c.push_back(-t * a[i + 1] / a[i]);
-      c.push_back(t * a[i] / a[i + 1]);
-      a[i] *= co;
-      a[i + 1] *= co;
-    }
-  }
-  for (int i = 0; i < n; ++i) c.push_back(a[i] * gain);
-  return true;
+// scaled-rotation packing of a Givens schedule: givens_pack.h (host only, shared with
+// the CPU unit test of the butterflies)
+static bool pack_givens2(const dctadj_axis* ax, bool inverse, double gain, int base_before,
+                         std::vector<double>& c) {
+  return pack_givens2(ax->n, ax->taps, ax->givens, inverse, gain, base_before, c);
 }
 
 static void pack_sub(const dctadj_axis* ax, bool transpose, int k, std::vector<double>& c) {
@@ -344,10 +323,14 @@ static int plan_axis(const dctadj_axis* ax, bool inverse, bool force_dense, Axis
   // trails the base for the inverse PRE / forward POST order, where the base's
   // gain sqrt(n) is folded into the final scales
   const bool adj_first = (ax->side == DCTADJ_SIDE_PRE) != inverse;
+  const double ggain = adj_first ? 1.0 : 1.0 / std::sqrt(static_cast<double>(ax->n));
+  const bool defer32 = !adj_first && deferred_policy(false, ax->n);
+  const bool defer64 = !adj_first && deferred_policy(true, ax->n);
+  p->coef64.clear();
   if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps == 4 || ax->taps == 6) && ax->givens &&
       ax->ngivens == givens_rots(ax->n, ax->taps) && !force_dense &&
-      pack_givens2(ax, inverse, adj_first ? 1.0 : 1.0 / std::sqrt(static_cast<double>(ax->n)),
-                   p->coef)) {
+      pack_givens2(ax, inverse, ggain, defer32 ? base : ST_NONE, p->coef)) {
+    if (defer64 != defer32) pack_givens2(ax, inverse, ggain, defer64 ? base : ST_NONE, p->coef64);
     adj_stage = ST_GIVENS2;
     k = ax->taps;
   } else if (ax->adj == DCTADJ_ADJ_BAND && (ax->taps == 4 || ax->taps == 6)) {
@@ -366,6 +349,7 @@ static int plan_axis(const dctadj_axis* ax, bool inverse, bool force_dense, Axis
     p->code = op_code(ST_DENSE);
     p->gain_sq = 1;
     p->coef.clear();
+    p->coef64.clear();
     return ST_OK;
   }
   p->gain_sq = ax->n;
@@ -380,6 +364,12 @@ static int plan_axis(const dctadj_axis* ax, bool inverse, bool force_dense, Axis
 }
 
 static size_t dt_size(int dtype) { return dtype == DT_F32 ? 4 : 8; }
+
+static std::vector<unsigned char> to_dtype(const std::vector<double>& v, int dtype);
+// an axis plan's coefficients for kernels of element type `dtype`
+static std::vector<unsigned char> plan_coef(const AxisPlan& p, int dtype) {
+  return to_dtype(dtype == DT_F64 && !p.coef64.empty() ? p.coef64 : p.coef, dtype);
+}
 
 // fp64 host coefficients -> the kernel's element type
 static std::vector<unsigned char> to_dtype(const std::vector<double>& v, int dtype) {
@@ -498,8 +488,8 @@ static int prepare(Launch& L, const AxisPlan& row, const AxisPlan* col, int dtyp
   const int cc = col ? col->code : op_code(ST_NONE);
   L.k = find_kernel(dtype, h, w, row.code, cc, col_first ? 1 : 0, in_mode, out_mode);
   if (!L.k) return ST_ERR_UNSUPPORTED;
-  L.row_coef = to_dtype(row.coef, dtype);
-  if (col) L.col_coef = to_dtype(col->coef, dtype);
+  L.row_coef = plan_coef(row, dtype);
+  if (col) L.col_coef = plan_coef(*col, dtype);
   int rc = upload_dense(row, dtype, st, &L.dense_row);
   if (rc) return rc;
   if (col) {
@@ -1059,8 +1049,8 @@ static int run_roundtrip(const dctadj_axis* h, const dctadj_axis* v, const void*
     if (!rc) rc = run_2d(h, v, y, xr, nblk, dtype, true, MODE_LINEAR, MODE_LINEAR, 0, 0, 0, st);
     return rc;
   }
-  const std::vector<unsigned char> c0 = to_dtype(fh.coef, dtype), c1 = to_dtype(fv.coef, dtype),
-                                   c2 = to_dtype(ih.coef, dtype), c3 = to_dtype(iv.coef, dtype);
+  const std::vector<unsigned char> c0 = plan_coef(fh, dtype), c1 = plan_coef(fv, dtype),
+                                   c2 = plan_coef(ih, dtype), c3 = plan_coef(iv, dtype);
   RtArgs a;
   a.coef[0] = c0.data();
   a.coef[1] = c1.data();
@@ -1310,7 +1300,7 @@ static int run_frames_exact(const dctadj_axis* h, const dctadj_axis* v, const dc
       if ((rc = upload_dense(peh, dtype, st, &L.dense_row)) ||
           (rc = upload_dense(pev, dtype, st, &L.dense_col)))
         return rc;
-      std::vector<unsigned char> rcf = to_dtype(ph.coef, DT_F32), ccf = to_dtype(pv.coef, DT_F32);
+      std::vector<unsigned char> rcf = plan_coef(ph, DT_F32), ccf = plan_coef(pv, DT_F32);
       LaunchArgs a;
       a.in = frames;
       a.out = exact;
@@ -1606,8 +1596,8 @@ static int run_mixed_roundtrip(const dctadj_mixed* plan, const dctadj_axis* tabl
   for (size_t i = 0; i < plan->classes.size(); ++i) {
     const auto& c = plan->classes[i];
     const MixedRtClass& r = runs[i];
-    const std::vector<unsigned char> c0 = to_dtype(r.fh.coef, dtype), c1 = to_dtype(r.fv.coef, dtype),
-                                     c2 = to_dtype(r.ih.coef, dtype), c3 = to_dtype(r.iv.coef, dtype);
+    const std::vector<unsigned char> c0 = plan_coef(r.fh, dtype), c1 = plan_coef(r.fv, dtype),
+                                     c2 = plan_coef(r.ih, dtype), c3 = plan_coef(r.iv, dtype);
     RtArgs a;
     a.in = x;
     a.y = y;

@@ -16,6 +16,7 @@
 //   sub   <- reference kernels/_fastcore.pyx:276-290 (leading BxB, tail untouched)
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "twiddles.h"
 
@@ -52,7 +53,7 @@ DA_DEV f2 sub(f2 a, f2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))
 DA_DEV f2 neg(f2 a) { return {make_float2(-a.v.x, -a.v.y)}; }
 DA_DEV f2 mul(f2 a, float c) { return {__fmul2_rn(a.v, make_float2(c, c))}; }
 DA_DEV f2 fmac(f2 a, float c, f2 b) { return {__ffma2_rn(a.v, make_float2(c, c), b.v)}; }
-DA_DEV f2 fnmac(f2 a, float c, f2 b) { return {__ffma2_rn(make_float2(-a.v.x, -a.v.y), make_float2(c, c), b.v)}; }
+DA_DEV f2 fnmac(f2 a, float c, f2 b) { return {__ffma2_rn(a.v, make_float2(-c, -c), b.v)}; }
 
 // Unnormalized recursion.  The reference scales by 1/sqrt(2) at every level
 // (u = (a+b)/sqrt2, v = (a-b)/sqrt2, and (c +- s)/sqrt2 in the DCT-4 output
@@ -65,7 +66,6 @@ DA_DEV f2 fnmac(f2 a, float c, f2 b) { return {__ffma2_rn(make_float2(-a.v.x, -a
 template <typename V, int N> DA_DEV void dct2u(const V (&x)[N], V (&y)[N]);
 template <typename V, int M> DA_DEV void dct4u(const V (&x)[M], V (&y)[M]);
 template <typename V, int N> DA_DEV void idct2u(const V (&y)[N], V (&x)[N]);
-template <typename V, int M> DA_DEV void idct4u(const V (&y)[M], V (&x)[M]);
 
 // DCT-2, gain sqrt(N): structure of reference _fastcore.pyx:50-84
 template <typename V, int N>
@@ -130,9 +130,247 @@ DA_DEV void dct4u(const V (&x)[M], V (&y)[M]) {
   y[2 * H - 1] = mul(s2[0], -SQ2);
 }
 
-// DCT-3 (inverse DCT-2), gain sqrt(N): structure of reference _fastcore.pyx:120-152
+// ---------------------------------------------------------------------------
+// Forward DCT-2 with DEFERRED scales (round 2; dct2d / dct4d).  In the forward
+// direction the rotations open the DCT-4, so their cosines cannot be absorbed by
+// a following add; instead every value carries a compile-time scale (held h,
+// true value s * h): an add / subtract of two values with scales a, b becomes
+// one FMA, h_a +- (b / a) h_b, with scale a; a rotation becomes two independent
+// FMAs whose results carry c * a and c * b; the sqrt2 multiplies of the DCT-4
+// end outputs disappear into their scales.  All ratios are constants, so a
+// 32-point transform is 186 instructions instead of 242 -- but its outputs come
+// out as y[k] = Dct2dOut<In, N>::at(k) * held[k], so it is used only in front of
+// a stage that takes per-sample input scales for free: the scaled-rotation band
+// stage (ST_GIVENS2: the host starts its scale tracking from dct2d_out_scales).
+// `In` types give the input scales: ScUnit, or ScAlt for the sign alternation
+// of idst3 (a free negation).
+struct ScUnit {
+  static __host__ __device__ constexpr double at(int) { return 1.0; }
+};
+struct ScAlt {
+  static __host__ __device__ constexpr double at(int i) { return i % 2 ? -1.0 : 1.0; }
+};
+template <class In, int M>
+struct ScRotP {  // p = cp a + sp b = (cp a_s) (A + rho B)
+  static __host__ __device__ constexpr double at(int n) { return psi_c(psi_off(M) + n) * In::at(n); }
+};
+template <class In, int M>
+struct ScRotQ {  // (+-) q = (+-) (cp b - sp a) = (+-)(cp b_s) (B - rho A): DST-2 sign alternation in the scale
+  static __host__ __device__ constexpr double at(int n) {
+    return (n % 2 ? -1.0 : 1.0) * psi_c(psi_off(M) + n) * In::at(M - 1 - n);
+  }
+};
+template <class In, int N> struct Dct2dOut;
+template <class In, int M>
+struct Dct4dOut {
+  using C = Dct2dOut<ScRotP<In, M>, M / 2>;
+  using Q = Dct2dOut<ScRotQ<In, M>, M / 2>;
+  static __host__ __device__ constexpr double at(int k) {
+    return k == 0 ? K_SQRT2 * C::at(0) : k == M - 1 ? -K_SQRT2 * Q::at(0) : C::at((k + 1) / 2);
+  }
+};
+template <class In, int N>
+struct Dct2dOut {
+  static __host__ __device__ constexpr double at(int k) {
+    if constexpr (N == 1 || N == 2) {
+      return In::at(0);
+    } else if constexpr (N == 4) {
+      return k == 1 ? K_A4X2 * In::at(0) : k == 3 ? -K_A4X2 * In::at(1) : In::at(0);
+    } else {
+      return k % 2 == 0 ? Dct2dOut<In, N / 2>::at(k / 2) : Dct4dOut<In, N / 2>::at(k / 2);
+    }
+  }
+};
+
+template <int I, int E, class F>
+DA_DEV void static_for(F&& f) {
+  if constexpr (I < E) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, E>(f);
+  }
+}
+
+// sum = a + r b, diff = a - r b for a compile-time ratio (plain add / subtract when |r| = 1)
+#define DA_BFLY(a, b, r, sum, diff)        \
+  if constexpr ((r) == S(1)) {             \
+    sum = add(a, b);                       \
+    diff = sub(a, b);                      \
+  } else if constexpr ((r) == S(-1)) {     \
+    sum = sub(a, b);                       \
+    diff = add(a, b);                      \
+  } else {                                 \
+    sum = fmac(b, r, a);                   \
+    diff = fnmac(b, r, a);                 \
+  }
+
+template <typename V, class In, int N> DA_DEV void dct2d(const V (&x)[N], V (&y)[N]);
+
+template <typename V, class In, int M>
+DA_DEV void dct4d(const V (&x)[M], V (&y)[M]) {
+  static_assert(M >= 4, "dct4d is only reached from dct2d with N >= 8");
+  using S = typename Scalar<V>::type;
+  constexpr int H = M / 2;
+  constexpr int OFF = psi_off(M);
+  using PS = ScRotP<In, M>;
+  using QS = ScRotQ<In, M>;
+  V p[H], sq[H], c[H], s2[H];
+  static_for<0, H>([&](auto ic) {
+    constexpr int n = decltype(ic)::value;
+    constexpr double t = psi_s(OFF + n) / psi_c(OFF + n), a = In::at(n), b = In::at(M - 1 - n);
+    constexpr S rp = S(t * b / a), rq = S(t * a / b);
+    p[n] = fmac(x[M - 1 - n], rp, x[n]);
+    sq[n] = fnmac(x[n], rq, x[M - 1 - n]);
+  });
+  dct2d<V, PS, H>(p, c);
+  dct2d<V, QS, H>(sq, s2);
+  using CO = Dct2dOut<PS, H>;
+  using QO = Dct2dOut<QS, H>;
+  y[0] = c[0];
+  static_for<1, H>([&](auto ic) {
+    constexpr int r = decltype(ic)::value;
+    constexpr S rho = S(QO::at(H - r) / CO::at(r));
+    DA_BFLY(c[r], s2[H - r], rho, y[2 * r], y[2 * r - 1])
+  });
+  y[2 * H - 1] = s2[0];
+}
+
+template <typename V, class In, int N>
+DA_DEV void dct2d(const V (&x)[N], V (&y)[N]) {
+  using S = typename Scalar<V>::type;
+  if constexpr (N == 1) {
+    y[0] = x[0];
+  } else if constexpr (N == 2) {
+    constexpr S r = S(In::at(1) / In::at(0));
+    DA_BFLY(x[0], x[1], r, y[0], y[1])
+  } else if constexpr (N == 4) {
+    constexpr double a0 = In::at(0), a1 = In::at(1), a2 = In::at(2), a3 = In::at(3);
+    constexpr double BA = K_B4X2 / K_A4X2;
+    constexpr S r03 = S(a3 / a0), r12 = S(a2 / a1), r10 = S(a1 / a0);
+    V s03, d03, s12, d12;
+    DA_BFLY(x[0], x[3], r03, s03, d03)  // scale a0
+    DA_BFLY(x[1], x[2], r12, s12, d12)  // scale a1
+    DA_BFLY(s03, s12, r10, y[0], y[2])  // a0
+    y[1] = fmac(d12, S(BA * a1 / a0), d03);           // A a0 (d03 + (B a1 / A a0) d12)
+    y[3] = fnmac(d03, S(BA * a0 / a1), d12);          // -A a1 (d12 - (B a0 / A a1) d03)
+  } else {
+    constexpr int H = N / 2;
+    V u[H], v[H], eu[H], ov[H];
+    static_for<0, H>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      constexpr S r = S(In::at(N - 1 - i) / In::at(i));
+      DA_BFLY(x[i], x[N - 1 - i], r, u[i], v[i])
+    });
+    dct2d<V, In, H>(u, eu);
+    dct4d<V, In, H>(v, ov);
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      y[2 * i] = eu[i];
+      y[2 * i + 1] = ov[i];
+    }
+  }
+}
+
+// y[k] = dct2d_out_scale<N, ALT>(k) * held[k] after dct2d<V, ScUnit | ScAlt, N> (host: the
+// initial scales of the Givens stage that follows)
+template <int N, bool ALT>
+__host__ __device__ constexpr double dct2d_out_scale(int k) {
+  return ALT ? Dct2dOut<ScAlt, N>::at(k) : Dct2dOut<ScUnit, N>::at(k);
+}
+
+// Scaled rotations (round 2).  A DCT-4 pair rotation (c, s) = (cos psi, sin psi) is
+// c * [[1, -t], [t, 1]] with t = tan psi < 1: two independent FMAs once the factor
+// c is carried as a scale of both outputs.  In the inverse (DCT-3) direction the
+// rotations are the LAST step of the inverse DCT-4 and its outputs only feed the parent's
+// add / subtract butterflies, x = u +- v: with v = c v' those become FMAs, so the
+// scale costs nothing (2 instructions per rotation instead of 4; 46 of the 242 of
+// a 32-point transform).  idct4s returns v' and idct4_scale<M>(i) the factor of
+// output i (negative where the reference's sign alternation lands).
+template <int M>
+__host__ __device__ constexpr double idct4_scale(int i) {
+  const int n = i < M / 2 ? i : M - 1 - i;
+  const double c = psi_c(psi_off(M) + n);
+  return (i >= M / 2 && n % 2 == 1) ? -c : c;
+}
+template <typename V, int M> DA_DEV void idct4s(const V (&y)[M], V (&x)[M]);
+template <typename V, int N> DA_DEV void idct2s(const V (&y)[N], V (&x)[N]);
+template <typename V, int N> DA_DEV void idct2p(const V (&y)[N], V (&x)[N]);
+
+// DCT-3 (inverse DCT-2), gain sqrt(N), scaled rotations: structure of reference _fastcore.pyx:120-152
 template <typename V, int N>
-DA_DEV void idct2u(const V (&y)[N], V (&x)[N]) {
+DA_DEV void idct2s(const V (&y)[N], V (&x)[N]) {
+  using S = typename Scalar<V>::type;
+  if constexpr (N == 1) {
+    x[0] = y[0];
+  } else if constexpr (N == 2) {
+    x[0] = add(y[0], y[1]);
+    x[1] = sub(y[0], y[1]);
+  } else if constexpr (N == 4) {
+    // d03 = A y1 + B y3 = A (y1 + R y3), d12 = B y1 - A y3 = -A (y3 - R y1), R = B / A
+    constexpr S A = S(K_A4X2), R = S(K_B4X2 / K_A4X2);
+    const V s03 = add(y[0], y[2]), s12 = sub(y[0], y[2]);
+    const V d03 = fmac(y[3], R, y[1]);
+    const V d12 = fnmac(y[1], R, y[3]);
+    x[0] = fmac(d03, A, s03);
+    x[3] = fnmac(d03, A, s03);
+    x[1] = fnmac(d12, A, s12);
+    x[2] = fmac(d12, A, s12);
+  } else {
+    constexpr int H = N / 2;
+    V ye[H], yo[H], u[H], v[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      ye[i] = y[2 * i];
+      yo[i] = y[2 * i + 1];
+    }
+    idct2s<V, H>(ye, u);
+    idct4s<V, H>(yo, v);
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const S c = S(idct4_scale<H>(i));
+      x[i] = fmac(v[i], c, u[i]);
+      x[N - 1 - i] = fnmac(v[i], c, u[i]);
+    }
+  }
+}
+
+// inverse DCT-4 without the rotations' cosines (x[i] = idct4_scale<M>(i) * out[i]),
+// gain sqrt(M): structure of reference _fastcore.pyx:155-185
+template <typename V, int M>
+DA_DEV void idct4s(const V (&y)[M], V (&x)[M]) {
+  static_assert(M >= 4, "idct4s is only reached from idct2s with N >= 8");
+  using S = typename Scalar<V>::type;
+  constexpr int H = M / 2;
+  constexpr int OFF = psi_off(M);
+  constexpr S SQ2 = S(K_SQRT2);
+  V c[H], sr[H], p[H], q[H];
+  c[0] = mul(y[0], SQ2);
+#pragma unroll
+  for (int r = 1; r < H; ++r) {
+    c[r] = add(y[2 * r], y[2 * r - 1]);
+    sr[H - r] = sub(y[2 * r], y[2 * r - 1]);  // s[r-1], stored reversed
+  }
+  sr[0] = mul(y[2 * H - 1], -SQ2);            // s[H-1]
+  idct2s<V, H>(c, p);
+  // inverse DST2: reverse, inverse DCT2, sign-alternate (folded into the rotation)
+  idct2s<V, H>(sr, q);
+#pragma unroll
+  for (int n = 0; n < H; ++n) {
+    const S t = S(psi_s(OFF + n) / psi_c(OFF + n));
+    if (n % 2 == 0) {  // cp (p - t q), cp (q + t p)
+      x[n] = fnmac(q[n], t, p[n]);
+      x[M - 1 - n] = fmac(p[n], t, q[n]);
+    } else {           // cp (p + t q), -cp (q - t p)
+      x[n] = fmac(q[n], t, p[n]);
+      x[M - 1 - n] = fnmac(p[n], t, q[n]);
+    }
+  }
+}
+
+template <typename V, int M> DA_DEV void idct4p(const V (&y)[M], V (&x)[M]);
+// DCT-3 (inverse DCT-2), gain sqrt(N), plain rotations (2 multiplies + 2 FMAs each):
+// structure of reference _fastcore.pyx:120-152
+template <typename V, int N>
+DA_DEV void idct2p(const V (&y)[N], V (&x)[N]) {
   using S = typename Scalar<V>::type;
   if constexpr (N == 1) {
     x[0] = y[0];
@@ -156,8 +394,8 @@ DA_DEV void idct2u(const V (&y)[N], V (&x)[N]) {
       ye[i] = y[2 * i];
       yo[i] = y[2 * i + 1];
     }
-    idct2u<V, H>(ye, u);
-    idct4u<V, H>(yo, v);
+    idct2p<V, H>(ye, u);
+    idct4p<V, H>(yo, v);
 #pragma unroll
     for (int i = 0; i < H; ++i) {
       x[i] = add(u[i], v[i]);
@@ -168,8 +406,8 @@ DA_DEV void idct2u(const V (&y)[N], V (&x)[N]) {
 
 // inverse DCT-4, gain sqrt(M): structure of reference _fastcore.pyx:155-185
 template <typename V, int M>
-DA_DEV void idct4u(const V (&y)[M], V (&x)[M]) {
-  static_assert(M >= 4, "idct4u is only reached from idct2u with N >= 8");
+DA_DEV void idct4p(const V (&y)[M], V (&x)[M]) {
+  static_assert(M >= 4, "idct4p is only reached from idct2p with N >= 8");
   using S = typename Scalar<V>::type;
   constexpr int H = M / 2;
   constexpr int OFF = psi_off(M);
@@ -182,9 +420,9 @@ DA_DEV void idct4u(const V (&y)[M], V (&x)[M]) {
     sr[H - r] = sub(y[2 * r], y[2 * r - 1]);  // s[r-1], stored reversed
   }
   sr[0] = mul(y[2 * H - 1], -SQ2);            // s[H-1]
-  idct2u<V, H>(c, p);
+  idct2p<V, H>(c, p);
   // inverse DST2: reverse, inverse DCT2, sign-alternate (folded into the rotation)
-  idct2u<V, H>(sr, q);
+  idct2p<V, H>(sr, q);
 #pragma unroll
   for (int n = 0; n < H; ++n) {
     const S cp = S(psi_c(OFF + n)), sp = S(psi_s(OFF + n));
@@ -196,6 +434,47 @@ DA_DEV void idct4u(const V (&y)[M], V (&x)[M]) {
       x[M - 1 - n] = fnmac(q[n], cp, mul(p[n], sp));
     }
   }
+}
+
+
+// Which form a kernel gets is a per-(type, size) choice, measured on the B200 (A/B
+// libraries, profiles/r02_tuning.md): fp32 (scalar and packed) up to 32 points runs
+// the scaled / deferred forms (fused round trips: config 2 +1.4 %, config 3 pre
+// +5.6 %, post +1.5 %); fp64 (config 1: +4 % time) and the 64-point kernels (config
+// 4's ring kernel: instruction-fetch stalls double, forward +3 %, inverse +12 %) keep
+// the plain forms.  The choice depends on (type, size) only, never on the kernel
+// family, so every kernel that computes the same transform stays bit-identical.
+// DCTADJ_IDCT_SCALED / DCTADJ_DEFERRED = 0 build the plain forms everywhere.
+#ifndef DCTADJ_IDCT_SCALED
+#define DCTADJ_IDCT_SCALED 1
+#endif
+#ifndef DCTADJ_DEFERRED
+#define DCTADJ_DEFERRED 1
+#endif
+#ifndef DCTADJ_SCALED_MAXN
+#define DCTADJ_SCALED_MAXN 32
+#endif
+__host__ __device__ constexpr bool idct_scaled_policy(bool is_double, int n) {
+  return DCTADJ_IDCT_SCALED != 0 && !is_double && n <= DCTADJ_SCALED_MAXN;
+}
+__host__ __device__ constexpr bool deferred_policy(bool is_double, int n) {
+  return DCTADJ_DEFERRED != 0 && !is_double && n <= DCTADJ_SCALED_MAXN;
+}
+template <typename V, int N>
+__host__ __device__ constexpr bool use_idct_scaled() {
+  return idct_scaled_policy(std::is_same<V, double>::value, N);
+}
+template <typename S, int N>
+__host__ __device__ constexpr bool use_deferred() {
+  return deferred_policy(std::is_same<S, double>::value, N);
+}
+
+template <typename V, int N>
+DA_DEV void idct2u(const V (&y)[N], V (&x)[N]) {
+  if constexpr (use_idct_scaled<V, N>())
+    idct2s<V, N>(y, x);
+  else
+    idct2p<V, N>(y, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -267,6 +546,10 @@ struct AxisOp {
   // 1/sqrt(N) already (the host folds it in)
   static constexpr bool kBase = (S1 >= ST_DCT2 && S1 <= ST_IDST3) || (S2 >= ST_DCT2 && S2 <= ST_IDST3);
   static constexpr int kGainSq = (kBase && S2 != ST_GIVENS2) ? N : 1;  // gain^2
+  // a forward-direction base (dct2 / idst3) in front of the scaled-rotation band runs
+  // with deferred scales (dct2d): the band's input scales absorb them on the host
+  static constexpr bool kDeferred =
+      (S1 == ST_DCT2 || S1 == ST_IDST3) && S2 == ST_GIVENS2 && use_deferred<T, N>();
   struct Coef {
     T c[NCOEF > 0 ? NCOEF : 1];
   };
@@ -367,12 +650,32 @@ DA_DEV void run_stage(V (&v)[N], const typename Scalar<V>::type* __restrict__ cf
   }
 }
 
+// Output scales of the deferred base in front of a Givens stage (host side: the
+// initial running scales of pack_givens2): v[j] = deferred_base_scale(...) * held[j].
+template <int N, int S1>
+__host__ __device__ constexpr double deferred_base_scale(int j) {
+  return S1 == ST_IDST3 ? dct2d_out_scale<N, true>(N - 1 - j) : dct2d_out_scale<N, false>(j);
+}
+
 template <typename V, int N, int CODE>
 DA_DEV void apply_axis(V (&v)[N],
                        const typename AxisOp<typename Scalar<V>::type, N, CODE>::Coef& cf,
                        const typename Scalar<V>::type* __restrict__ dense) {
   using Op = AxisOp<typename Scalar<V>::type, N, CODE>;
-  run_stage<V, N, Op::S1, Op::K>(v, cf.c, dense);
+  if constexpr (Op::kDeferred) {
+    V y[N];
+    if constexpr (Op::S1 == ST_IDST3) {  // negate odd (in the scales) -> dct2 -> reverse
+      dct2d<V, ScAlt, N>(v, y);
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = y[N - 1 - j];
+    } else {
+      dct2d<V, ScUnit, N>(v, y);
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = y[j];
+    }
+  } else {
+    run_stage<V, N, Op::S1, Op::K>(v, cf.c, dense);
+  }
   run_stage<V, N, Op::S2, Op::K>(v, cf.c, dense);
 }
 

@@ -10,12 +10,12 @@
 constexpr int ACC = 12;    // independent chains per thread
 constexpr int ITERS = 2048;
 
-enum Kind { FFMA_RRR, FFMA_RIR, FFMA_RUR, FADD_RR, FFMA2_RIR, FFMA2_RUR, FFMA2_RRR, FADD2_RR, FMUL2_RI, MIX_2D };
+enum Kind { FFMA_RRR, FFMA_RIR, FFMA_RUR, FADD_RR, FFMA2_RIR, FFMA2_RUR, FFMA2_RRR, FADD2_RR, FMUL2_RI, MIX_2D, MIX_HALF, MIX_SCALAR_HALF };
 
 template <int K>
 __global__ void __launch_bounds__(256) kern(float* out, float ku, float kv) {
   const float kr = ku + threadIdx.x * 1e-30f;  // a per-thread (vector register) value
-  if constexpr (K <= FADD_RR) {
+  if constexpr (K <= FADD_RR || K == MIX_SCALAR_HALF) {
     float a[ACC];
 #pragma unroll
     for (int i = 0; i < ACC; ++i) a[i] = threadIdx.x * 0.001f + i;
@@ -27,6 +27,10 @@ __global__ void __launch_bounds__(256) kern(float* out, float ku, float kv) {
         if constexpr (K == FFMA_RIR) a[i] = fmaf(a[i], 0.70710677f, a[(i + 1) % ACC]);
         if constexpr (K == FFMA_RUR) a[i] = fmaf(a[i], ku, a[(i + 1) % ACC]);
         if constexpr (K == FADD_RR) a[i] = a[i] + a[(i + 1) % ACC];
+        if constexpr (K == MIX_SCALAR_HALF) {
+          if (i % 2 == 0) a[i] = a[i] + a[(i + 1) % ACC];
+          else a[i] = fmaf(a[i], 0.70710677f, a[(i + 1) % ACC]);
+        }
       }
     }
     float s = 0;
@@ -47,6 +51,10 @@ __global__ void __launch_bounds__(256) kern(float* out, float ku, float kv) {
         if constexpr (K == FFMA2_RRR) a[i] = __ffma2_rn(a[i], kr2, a[(i + 1) % ACC]);
         if constexpr (K == FADD2_RR) a[i] = __fadd2_rn(a[i], a[(i + 1) % ACC]);
         if constexpr (K == FMUL2_RI) a[i] = __fmul2_rn(a[i], ki2);
+        if constexpr (K == MIX_HALF) {  // 1 FADD2 : 1 FFMA2-imm (do they share a pipe?)
+          if (i % 2 == 0) a[i] = __fadd2_rn(a[i], a[(i + 1) % ACC]);
+          else a[i] = __ffma2_rn(a[i], ki2, a[(i + 1) % ACC]);
+        }
         if constexpr (K == MIX_2D) {  // butterfly-like: add / sub / ffma-imm alternating
           if (i % 3 == 0) a[i] = __fadd2_rn(a[i], a[(i + 1) % ACC]);
           else if (i % 3 == 1) a[i] = __fadd2_rn(a[i], make_float2(-a[(i + 1) % ACC].x, -a[(i + 1) % ACC].y));
@@ -100,6 +108,8 @@ int main() {
   run<FADD2_RR>("FADD2 rr", out, p.multiProcessorCount, clk);
   run<FMUL2_RI>("FMUL2 ri", out, p.multiProcessorCount, clk);
   run<MIX_2D>("mix2", out, p.multiProcessorCount, clk);
+  run<MIX_HALF>("FADD2+FFMA2", out, p.multiProcessorCount, clk);
+  run<MIX_SCALAR_HALF>("FADD+FFMA", out, p.multiProcessorCount, clk);
   cudaError_t e = cudaDeviceSynchronize();
   std::printf("status: %s\n", cudaGetErrorString(e));
   return 0;
