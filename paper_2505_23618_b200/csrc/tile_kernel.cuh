@@ -646,6 +646,9 @@ __global__ void __launch_bounds__(NG * NW * 32, (CH >> 4) > 0 ? (CH >> 4) : 1)
 //     has been read (cp.async.bulk.wait_group.read 1)
 //   compute warp: waits full[s], row + column pass in place (packed pairs),
 //     fence.proxy.async, arrives done[s]
+#ifndef DCTADJ_RING_PAIR
+#define DCTADJ_RING_PAIR 1
+#endif
 template <typename T, int H, int W, int RC, int CC, bool COL_FIRST, int NC, int S>
 __global__ void __launch_bounds__((NC + 1) * 32, 1)
     ring_kernel(const __grid_constant__ CUtensorMap in_map,
@@ -719,6 +722,16 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
     // the wait below.
     if (k >= 1) mbar_wait(&done[s], static_cast<uint32_t>((k - 1) & 1));
     mbar_wait(&full[s], static_cast<uint32_t>(k & 1));
+    // Column-first (inverse) kernels: the two compute warps of an SM sub-partition (warps w
+    // and w + 4) start their tiles together, so they walk the straight-line pass code
+    // roughly in step and share its instruction fetches (the 64-point passes are ~75 KB of
+    // code and instruction fetch is this kernel's top stall): inverse -1.5..-3 %; the
+    // row-first kernels lose 14 % to it (both warps in their load / store phases at once)
+    // and run unpaired (profiles/r02_tuning.md).  Both warps have a tile in this round
+    // iff tile r * 8 + w + 4 exists.
+    if constexpr (COL_FIRST && NC == 8 && DCTADJ_RING_PAIR != 0) {
+      if (warp >= 4 || i + 4 < n) asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp & 3)) : "memory");
+    }
     if constexpr (!COL_FIRST) {
       row_pass<T, H, W, 1, RC, 1, true>(buf, lane, prm.row, nullptr);
       __syncwarp();
