@@ -649,6 +649,7 @@ __global__ void __launch_bounds__(NG * NW * 32, (CH >> 4) > 0 ? (CH >> 4) : 1)
 #ifndef DCTADJ_RING_PAIR
 #define DCTADJ_RING_PAIR 1
 #endif
+
 template <typename T, int H, int W, int RC, int CC, bool COL_FIRST, int NC, int S>
 __global__ void __launch_bounds__((NC + 1) * 32, 1)
     ring_kernel(const __grid_constant__ CUtensorMap in_map,
