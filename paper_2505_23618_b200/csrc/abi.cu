@@ -341,6 +341,14 @@ static int plan_axis(const dctadj_axis* ax, bool inverse, bool force_dense, Axis
     adj_stage = ST_SUB;
     k = 8;
     pack_sub(ax, inverse, k, p->coef);
+    // behind a deferred-scale DCT-2 (butterfly.cuh AxisOp::kDeferredSub) the block acts on
+    // held values: fold their scales into its columns (fp32 kernels; fp64 keeps the block)
+    if (!adj_first && base == ST_DCT2 && !force_dense && (defer32 || defer64)) {
+      std::vector<double> folded = p->coef;
+      fold_sub_scales(ax->n, k, folded);
+      if (defer64 != defer32) p->coef64 = defer64 ? folded : p->coef;
+      if (defer32) p->coef = folded;
+    }
   } else if (ax->adj != DCTADJ_ADJ_NONE) {
     force_dense = true;
   }

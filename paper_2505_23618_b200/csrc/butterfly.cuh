@@ -270,6 +270,22 @@ DA_DEV void dct2d(const V (&x)[N], V (&y)[N]) {
   }
 }
 
+// out[k] = scale_k * held[k] for k >= FROM (one multiply, none where the scale is 1);
+// REV: out[j] = the value of held[N - 1 - j] (idst3's output reversal)
+template <typename V, class In, int N, int FROM, bool REV>
+DA_DEV void finalize_deferred(const V (&held)[N], V (&out)[N]) {
+  using S = typename Scalar<V>::type;
+  static_for<FROM, N>([&](auto ic) {
+    constexpr int k = decltype(ic)::value;
+    constexpr double sg = Dct2dOut<In, N>::at(k);
+    constexpr int o = REV ? N - 1 - k : k;
+    if constexpr (sg == 1.0)
+      out[o] = held[k];
+    else
+      out[o] = mul(held[k], S(sg));
+  });
+}
+
 // y[k] = dct2d_out_scale<N, ALT>(k) * held[k] after dct2d<V, ScUnit | ScAlt, N> (host: the
 // initial scales of the Givens stage that follows)
 template <int N, bool ALT>
@@ -550,6 +566,9 @@ struct AxisOp {
   // with deferred scales (dct2d): the band's input scales absorb them on the host
   static constexpr bool kDeferred =
       (S1 == ST_DCT2 || S1 == ST_IDST3) && S2 == ST_GIVENS2 && use_deferred<T, N>();
+  // dct2 in front of the sub-block post-adjustment: the host folds the deferred scales of
+  // the K adjusted inputs into the block's columns; the untouched tail is finalized
+  static constexpr bool kDeferredSub = S1 == ST_DCT2 && S2 == ST_SUB && use_deferred<T, N>();
   struct Coef {
     T c[NCOEF > 0 ? NCOEF : 1];
   };
@@ -558,13 +577,22 @@ struct AxisOp {
 template <typename V, int N, int S, int K>
 DA_DEV void run_stage(V (&v)[N], const typename Scalar<V>::type* __restrict__ cf,
                       const typename Scalar<V>::type* __restrict__ dense) {
+  using Sc = typename Scalar<V>::type;
   if constexpr (S == ST_NONE) {
     return;
   } else if constexpr (S == ST_DCT2) {
     V y[N];
-    dct2u<V, N>(v, y);
+    if constexpr (use_deferred<Sc, N>()) {
+      // deferred-scale form, finalized: one multiply per output whose scale is not 1
+      // (186 + 30 instead of 242 at 32 points).  The sub-block post-adjustment below
+      // (apply_axis) finalizes its untouched tail the same way, bit for bit.
+      dct2d<V, ScUnit, N>(v, y);
+      finalize_deferred<V, ScUnit, N, 0, false>(y, v);
+    } else {
+      dct2u<V, N>(v, y);
 #pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = y[i];
+      for (int i = 0; i < N; ++i) v[i] = y[i];
+    }
   } else if constexpr (S == ST_IDCT2) {
     V y[N];
     idct2u<V, N>(v, y);
@@ -579,11 +607,16 @@ DA_DEV void run_stage(V (&v)[N], const typename Scalar<V>::type* __restrict__ cf
     for (int j = 0; j < N; ++j) v[j] = (j % 2 == 0) ? y[j] : neg(y[j]);
   } else if constexpr (S == ST_IDST3) {
     V a[N], y[N];
+    if constexpr (use_deferred<Sc, N>()) {
+      dct2d<V, ScAlt, N>(v, y);  // the sign alternation is an input scale of -1
+      finalize_deferred<V, ScAlt, N, 0, true>(y, v);
+    } else {
 #pragma unroll
-    for (int j = 0; j < N; ++j) a[j] = (j % 2 == 0) ? v[j] : neg(v[j]);
-    dct2u<V, N>(a, y);
+      for (int j = 0; j < N; ++j) a[j] = (j % 2 == 0) ? v[j] : neg(v[j]);
+      dct2u<V, N>(a, y);
 #pragma unroll
-    for (int j = 0; j < N; ++j) v[j] = y[N - 1 - j];
+      for (int j = 0; j < N; ++j) v[j] = y[N - 1 - j];
+    }
   } else if constexpr (S == ST_BAND) {
     constexpr int D = 2 * K - 1;
     V y[N];
@@ -662,7 +695,20 @@ DA_DEV void apply_axis(V (&v)[N],
                        const typename AxisOp<typename Scalar<V>::type, N, CODE>::Coef& cf,
                        const typename Scalar<V>::type* __restrict__ dense) {
   using Op = AxisOp<typename Scalar<V>::type, N, CODE>;
-  if constexpr (Op::kDeferred) {
+  if constexpr (Op::kDeferredSub) {
+    constexpr int K = Op::K;
+    V y[N];
+    dct2d<V, ScUnit, N>(v, y);
+#pragma unroll
+    for (int r = 0; r < K; ++r) {  // cf = block * diag(scale_0..K-1): acts on the held values
+      V acc = mul(y[0], cf.c[r * K]);
+#pragma unroll
+      for (int j = 1; j < K; ++j) acc = fmac(y[j], cf.c[r * K + j], acc);
+      v[r] = acc;
+    }
+    finalize_deferred<V, ScUnit, N, K, false>(y, v);
+    return;
+  } else if constexpr (Op::kDeferred) {
     V y[N];
     if constexpr (Op::S1 == ST_IDST3) {  // negate odd (in the scales) -> dct2 -> reverse
       dct2d<V, ScAlt, N>(v, y);

@@ -61,4 +61,11 @@ inline bool pack_givens2(int n, int k, const double* givens, bool inverse, doubl
   return true;
 }
 
+// Sub-block post-adjustment behind a deferred-scale DCT-2 (AxisOp::kDeferredSub): the k x k
+// block acts on held values, so the scales of its k inputs are folded into its columns.
+inline void fold_sub_scales(int n, int k, std::vector<double>& block) {
+  for (int r = 0; r < k; ++r)
+    for (int j = 0; j < k; ++j) block[r * k + j] *= deferred_scale_of<ST_DCT2>(n, j);
+}
+
 }  // namespace dctadj

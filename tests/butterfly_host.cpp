@@ -69,6 +69,10 @@ static int run_n(int s1, int s2, int k, int vtype, const double* coef, const dou
   CASE(ST_IDCT2, ST_NONE, 0)
   CASE(ST_DST3, ST_NONE, 0)
   CASE(ST_IDST3, ST_NONE, 0)
+  if constexpr (N >= 8) {
+    CASE(ST_DCT2, ST_SUB, 8)
+    CASE(ST_SUB, ST_IDCT2, 8)
+  }
   if constexpr (N >= 16) {
     CASE(ST_GIVENS2, ST_DST3, 6)
     CASE(ST_IDST3, ST_GIVENS2, 6)
@@ -107,6 +111,12 @@ int bf_pack_givens2(int n, int k, const double* givens, int inverse, double gain
 // the deferred-scale base in front of a Givens stage / the scaled inverse rotations
 int bf_deferred_policy(int is_double, int n) { return deferred_policy(is_double != 0, n); }
 int bf_idct_scaled_policy(int is_double, int n) { return idct_scaled_policy(is_double != 0, n); }
+// abi.cu's rule for an 8 x 8 block behind the deferred DCT-2 (in place)
+void bf_fold_sub(int n, int k, double* block) {
+  std::vector<double> b(block, block + k * k);
+  fold_sub_scales(n, k, b);
+  std::memcpy(block, b.data(), b.size() * sizeof(double));
+}
 double bf_deferred_scale(int n, int s1, int j) {
   return s1 == ST_IDST3 ? deferred_scale_of<ST_IDST3>(n, j) : deferred_scale_of<ST_DCT2>(n, j);
 }

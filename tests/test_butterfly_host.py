@@ -35,6 +35,8 @@ def bf(tmp_path_factory):
     lib.bf_deferred_scale.argtypes = [ctypes.c_int] * 3
     lib.bf_dct2d.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P]
     lib.bf_idct2.argtypes = [ctypes.c_int, ctypes.c_int, P, P]
+    lib.bf_fold_sub.argtypes = [ctypes.c_int, ctypes.c_int, P]
+    lib.bf_fold_sub.restype = None
     return lib
 
 
@@ -159,3 +161,32 @@ def test_flipped_dct8_pre_axis_with_deferred_base(bf, vtype):
     coef = _pack(bf, n, k, ang, True, 1.0 / np.sqrt(n), _before(bf, vtype, n, ST_DCT2))
     inv = apply(bf, n, ST_DCT2, ST_GIVENS2, k, vtype, coef, want)
     assert rel(inv, x) < 5 * TOL[vtype]
+
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
+@pytest.mark.parametrize("vtype", [0, 1, 2])
+def test_post_adjusted_axis_with_deferred_base(bf, n, vtype):
+    """Forward post (deferred DCT-2 -> 8x8 block with the held inputs' scales folded into its
+    columns, tail finalized) and inverse post (block^T -> scaled inverse DCT-2) against the
+    oracle; the untouched tail equals the kernel's own plain DCT-2 output bit for bit, and an
+    identity block reproduces the plain DCT-2 everywhere (the kernels' invariants)."""
+    ST_SUB = 6
+    name = f"sub8_post_dct2_dst7_n{max(n, 16)}"
+    blk = np.ascontiguousarray(np.array(matio.load_designed(name).realized)[:8, :8])
+    x = np.random.default_rng(3).standard_normal((4, n)) * 30
+    plain = apply(bf, n, ST_DCT2, ST_NONE, 0, vtype, None, x)
+
+    def fwd(block):
+        c = np.ascontiguousarray(block, dtype=np.float64).copy()
+        if bf.bf_deferred_policy(int(vtype == 1), n):
+            bf.bf_fold_sub(n, 8, _p(c))
+        return apply(bf, n, ST_DCT2, ST_SUB, 8, vtype, c.ravel(), x)
+
+    y = fwd(blk)
+    want = O.dct2(x)
+    want[:, :8] = want[:, :8] @ blk.T
+    assert rel(y / np.sqrt(n), want) < TOL[vtype]
+    assert np.array_equal(y[:, 8:], plain[:, 8:])
+    assert np.array_equal(fwd(np.eye(8)), plain)
+    inv = apply(bf, n, ST_SUB, ST_IDCT2, 8, vtype, np.ascontiguousarray(blk.T).ravel(), want)
+    assert rel(inv / np.sqrt(n), x) < 5 * TOL[vtype]
