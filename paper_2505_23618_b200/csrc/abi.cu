@@ -743,6 +743,8 @@ static int launch_dense_tc(const LaunchArgs& a, int64_t nblocks, int tiles_y, in
   if constexpr (FRC != 0) {
     if (!fz) return fail(ST_ERR_VALUE, "fused launch without its arguments");
     if ((rc = make_map<float, 32, 32, 4, MODE_LINEAR_IL>(&adj_map, fz->adj_out, la))) return rc;
+    // the exact output is staged as an interleaved tile too (dense_tc.cuh, fused)
+    if ((rc = make_map<float, 32, 32, 4, MODE_LINEAR_IL>(&out_map, a.out, la))) return rc;
     using RowOp = AxisOp<float, 32, FRC>;
     using ColOp = AxisOp<float, 32, FCC>;
     if (RowOp::NCOEF > 0) std::memcpy(kp.row.c, fz->row_coef, sizeof(float) * RowOp::NCOEF);

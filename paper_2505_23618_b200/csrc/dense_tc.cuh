@@ -444,9 +444,21 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
       tc::fence_after();
       ev(k, 3);
       tc::ld32(ta + 64, v);
+      // Fused: from here on TMEM lane rho = 32 b + lane stands for the row of the INTERLEAVED
+      // tile (block rho & 3, block row rho >> 2), the layout of the adjusted tile in the ring
+      // stage, so the error pass below reads its Y_a row -- and stages its Y_e row -- at
+      // consecutive tile rows per lane (conflict-free; with lane = block row the 8 lanes of
+      // an LDS.128 phase hit 2 swizzle columns: 16 wavefronts instead of 4, a quarter of
+      // the kernel's shared-memory traffic).  The W transpose therefore goes through the
+      // whole group tile (rows 4 r + b) and a group barrier instead of a per-warp tile.
+      constexpr bool IL = FUSED;
 #pragma unroll
-      for (int r = 0; r < 32; ++r) *reinterpret_cast<uint32_t*>(gt + tc::sw(b * 32 + r, lane)) = v[r];
-      __syncwarp();
+      for (int r = 0; r < 32; ++r)
+        *reinterpret_cast<uint32_t*>(gt + tc::sw(IL ? r * 4 + b : b * 32 + r, lane)) = v[r];
+      if constexpr (IL)
+        group_bar();
+      else
+        __syncwarp();
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint4 w = *reinterpret_cast<const uint4*>(gt + tc::sw(b * 32 + lane, q * 4));
@@ -480,7 +492,7 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
         float d2 = 0.f, e2 = 0.f;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 a = *reinterpret_cast<const float4*>(x + tc::sw(lane * 4 + b, q * 4));
+          const float4 a = *reinterpret_cast<const float4*>(x + tc::sw(gl, q * 4));
           const float ya[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -505,13 +517,16 @@ __global__ void __launch_bounds__((4 * NGRP + 3) * 32, 1)
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<uint4*>(gt + tc::sw(tc_row<OUT_MODE>(b, lane), q * 4)) =
+        *reinterpret_cast<uint4*>(gt + tc::sw(FUSED ? gl : tc_row<OUT_MODE>(b, lane), q * 4)) =
             make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       fence_proxy_async_smem();
       tc::fence_before();
       group_bar();
       if (leader) {
-        tc_tile_io<OUT_MODE>(false, gt, &out_map, nullptr, t, geom);
+        if constexpr (FUSED)  // interleaved tile -> block-major memory (out_map: LINEAR_IL view)
+          tma_store_3d(&out_map, gt, 0, static_cast<int>(4 * t), 0);
+        else
+          tc_tile_io<OUT_MODE>(false, gt, &out_map, nullptr, t, geom);
         bulk_commit();
       }
       ev(k, 6);
