@@ -109,7 +109,8 @@ constexpr int kG8I = op_code(ST_DCT2, ST_GIVENS2, 6);
        RTGV(H, W, RF, CF, RI, CI, PRI, 2, 4, VAR + 3), RTGV(H, W, RF, CF, RI, CI, PRI, 4, 4, VAR + 4))
 #define RTGP(H, W, RF, CF, RI, CI) RTGV(H, W, RF, CF, RI, CI, false, 4, 2, 0)                    \
   TUNEC(RTGV(H, W, RF, CF, RI, CI, true, 4, 4, 1), RTGV(H, W, RF, CF, RI, CI, true, 4, 2, 2),      \
-       RTGV(H, W, RF, CF, RI, CI, false, 2, 4, 3), RTGV(H, W, RF, CF, RI, CI, false, 1, 8, 4))
+       RTGV(H, W, RF, CF, RI, CI, false, 2, 4, 3), RTGV(H, W, RF, CF, RI, CI, false, 1, 8, 4),     \
+       RTGV(H, W, RF, CF, RI, CI, false, 3, 3, 5), RTGV(H, W, RF, CF, RI, CI, true, 3, 3, 6))
 #define RT(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, VAR) \
   RTW(T, DT, H, W, P, RF, CF, RI, CI, NG, S, PRF, PC, PRI, MINB, YSTG, 1, VAR)
 
