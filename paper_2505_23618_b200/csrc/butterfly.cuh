@@ -14,6 +14,12 @@
 //   idst3 <- reference kernels/_fastcore.pyx:233-250 (negate odd, dct2, reverse)
 //   band  <- reference kernels/_fastcore.pyx:253-273 (ascending-j in-band sum)
 //   sub   <- reference kernels/_fastcore.pyx:276-290 (leading BxB, tail untouched)
+// Two forms of each butterfly live here: the plain ones (dct2u / dct4u, idct2p / idct4p:
+// the reference's rotations as 2 multiplies + 2 FMAs) and the scaled ones (idct2s / idct4s:
+// cosines absorbed by the parent's butterflies; dct2d / dct4d: compile-time deferred scales
+// absorbed by the stage behind, or finalized with one multiply per output).  Which one a
+// kernel gets is decided by (element type, size) alone -- idct_scaled_policy /
+// deferred_policy -- so every kernel family computes a transform with the same arithmetic.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -269,6 +275,8 @@ DA_DEV void dct2d(const V (&x)[N], V (&y)[N]) {
     }
   }
 }
+
+#undef DA_BFLY
 
 // out[k] = scale_k * held[k] for k >= FROM (one multiply, none where the scale is 1);
 // REV: out[j] = the value of held[N - 1 - j] (idst3's output reversal)
@@ -606,11 +614,12 @@ DA_DEV void run_stage(V (&v)[N], const typename Scalar<V>::type* __restrict__ cf
 #pragma unroll
     for (int j = 0; j < N; ++j) v[j] = (j % 2 == 0) ? y[j] : neg(y[j]);
   } else if constexpr (S == ST_IDST3) {
-    V a[N], y[N];
+    V y[N];
     if constexpr (use_deferred<Sc, N>()) {
       dct2d<V, ScAlt, N>(v, y);  // the sign alternation is an input scale of -1
       finalize_deferred<V, ScAlt, N, 0, true>(y, v);
     } else {
+      V a[N];
 #pragma unroll
       for (int j = 0; j < N; ++j) a[j] = (j % 2 == 0) ? v[j] : neg(v[j]);
       dct2u<V, N>(a, y);
