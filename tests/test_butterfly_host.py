@@ -190,3 +190,32 @@ def test_post_adjusted_axis_with_deferred_base(bf, n, vtype):
     assert np.array_equal(fwd(np.eye(8)), plain)
     inv = apply(bf, n, ST_SUB, ST_IDCT2, 8, vtype, np.ascontiguousarray(blk.T).ravel(), want)
     assert rel(inv / np.sqrt(n), x) < 5 * TOL[vtype]
+
+
+def _gain(n):
+    """tile_kernel.cuh inv_sqrt_pow2(n): 1 / sqrt(n) as the kernels apply it."""
+    e = int(np.log2(n))
+    return 0.5 ** (e // 2) * (0.7071067811865476 if e % 2 else 1.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_device_primitives_match_host_shim(bf, n, dtype):
+    """The B200 kernels and the host shim compile the SAME butterfly templates; the only
+    difference is nvcc contracting a multiply into a following add (-fmad) where g++ keeps two
+    roundings, so the four base primitives on the GPU equal the host-compiled templates to a
+    rounding or two -- far inside the parity bar -- which is what makes the CPU tests above
+    tests of the device arithmetic.  (The forward DCT-2 has no such pair: bit-identical.)"""
+    import torch
+    from paper_2505_23618_b200 import kernels
+    x = (np.random.default_rng(n).standard_normal((37, n)) * 30).astype(dtype)
+    vtype = 0 if dtype == np.float32 else 1
+    tol = 3e-7 if dtype == np.float32 else 1e-15
+    xd = torch.from_numpy(x).cuda()
+    for name, st in (("dct2", ST_DCT2), ("idct2", ST_IDCT2), ("dst3", ST_DST3), ("idst3", ST_IDST3)):
+        got = getattr(kernels, name)(xd).cpu().numpy()
+        held = apply(bf, n, st, ST_NONE, 0, vtype, None, x.astype(np.float64)).astype(dtype)
+        want = held * dtype(_gain(n))
+        assert got.dtype == dtype
+        assert rel(got.astype(np.float64), want.astype(np.float64)) < tol, (name, n, dtype)
