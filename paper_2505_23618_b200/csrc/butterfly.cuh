@@ -145,9 +145,12 @@ DA_DEV void dct4u(const V (&x)[M], V (&y)[M]) {
 // FMAs whose results carry c * a and c * b; the sqrt2 multiplies of the DCT-4
 // end outputs disappear into their scales.  All ratios are constants, so a
 // 32-point transform is 186 instructions instead of 242 -- but its outputs come
-// out as y[k] = Dct2dOut<In, N>::at(k) * held[k], so it is used only in front of
-// a stage that takes per-sample input scales for free: the scaled-rotation band
-// stage (ST_GIVENS2: the host starts its scale tracking from dct2d_out_scales).
+// out as y[k] = Dct2dOut<In, N>::at(k) * held[k].  Three consumers (apply_axis /
+// run_stage below): the scaled-rotation band stage takes per-sample input scales
+// for free (ST_GIVENS2: the host starts its scale tracking from them,
+// givens_pack.h); the sub-block post-adjustment gets them folded into its
+// block's columns by the host and finalizes only the untouched tail; a stage on
+// its own finalizes every output (one multiply where the scale is not 1: 216).
 // `In` types give the input scales: ScUnit, or ScAlt for the sign alternation
 // of idst3 (a free negation).
 struct ScUnit {
